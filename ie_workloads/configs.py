@@ -1,0 +1,208 @@
+"""The BASELINE.json configurations c1..c5 as concrete synthetic inputs.
+
+Grids are centred at the origin: origin_a = -(n_a - 1)/2 * h (centroid of cell (0,0,0)).
+Seed = config number.  Readings for the parts BASELINE.json leaves open are listed in
+DESIGN.md §Inputs; variants:
+  c2capped  sigma_h ~ 10^U[-2,0] instead of 10^U[-2,1] (the literal c2
+            contrast makes conventional-IE GMRES stagnate)
+  c3h, c4h  the c3 / c4 grids, contrast recipes and tools on a HOMOGENEOUS background
+            (sigma_b = 1 S/m, 400 kHz): the layered-table path (A3L) is not built yet.
+  *mini     the same recipe on an 8^3 grid so that dense LU gives exact truth.
+"""
+
+from dataclasses import dataclass, field
+from typing import Callable, List, Tuple
+
+import numpy as np
+
+from .generate import vti_tensor, haar_rotation, gaussian_random_field, tool_frame, box_grid
+
+
+@dataclass
+class Config:
+    name: str
+    n: Tuple[int, int, int]          # (nx, ny, nz)
+    h: float                         # cubic cell size, m
+    sigma_b: float                   # background conductivity, S/m
+    freq: float                      # Hz
+    seed: int
+    sigma_fn: Callable = None        # rng, cfg -> (nz, ny, nx, 3, 3) total sigma
+    sources: List = field(default_factory=list)    # [(pos(3), moment(3))]
+    receivers: List = field(default_factory=list)  # [pos(3)]
+    boxes: List = field(default_factory=list)      # [(i0,i1,j0,j1,k0,k1)]
+    restart: int = 30
+    outer_tol: float = 1e-8
+    parity_tol: float = 1e-9
+    note: str = ""
+
+    @property
+    def hvec(self):
+        return (self.h, self.h, self.h)
+
+    @property
+    def origin(self):
+        return tuple(-(na - 1) / 2.0 * self.h for na in self.n)
+
+    @property
+    def N(self):
+        return self.n[0] * self.n[1] * self.n[2]
+
+    def sigma(self):
+        rng = np.random.default_rng(self.seed)
+        return self.sigma_fn(rng, self)
+
+    def cell_centers(self, axis):
+        return self.origin[axis] + self.h * np.arange(self.n[axis])
+
+
+# ---------------------------------------------------------------------------- recipes
+
+def _c1_sigma(rng, cfg):
+    """c1: central block [n/4, 3n/4)^3, isotropic Delta sigma ~ U[0.5, 5] per cell (x-fastest)."""
+    nx, ny, nz = cfg.n
+    s = np.zeros((nz, ny, nx, 3, 3))
+    s[...] = cfg.sigma_b * np.eye(3)
+    a, b = nx // 4, 3 * nx // 4
+    d = rng.uniform(0.5, 5.0, size=(b - a, b - a, b - a))  # (z, y, x), x fastest
+    s[a:b, a:b, a:b] += d[..., None, None] * np.eye(3)
+    return s
+
+
+def _blocks_vti(rng, cfg, block, log_hi):
+    """c2: per block (x-fastest block order) draw sigma_h = 10^U[-2, log_hi], ratio U[0.1,1],
+    dip U[0,60] deg, azimuth U[0,360] deg, in that order; Appendix C tensor."""
+    nx, ny, nz = cfg.n
+    s = np.zeros((nz, ny, nx, 3, 3))
+    for kb in range(nz // block):
+        for jb in range(ny // block):
+            for ib in range(nx // block):
+                sh = 10.0 ** rng.uniform(-2.0, log_hi)
+                r = rng.uniform(0.1, 1.0)
+                th = np.radians(rng.uniform(0.0, 60.0))
+                ph = np.radians(rng.uniform(0.0, 360.0))
+                s[kb * block:(kb + 1) * block, jb * block:(jb + 1) * block, ib * block:(ib + 1) * block] = \
+                    vti_tensor(sh, r * sh, th, ph)
+    return s
+
+
+def _c3_sigma(rng, cfg, block=16):
+    """c3: one Haar rotation per block (x-fastest), then d_i = 10^U[-2, log10 5] per cell,
+    shape (nz, ny, nx, 3); sigma = R diag(d) R^T."""
+    nx, ny, nz = cfg.n
+    nbx, nby, nbz = -(-nx // block), -(-ny // block), -(-nz // block)
+    Rs = np.stack([haar_rotation(rng) for _ in range(nbx * nby * nbz)]).reshape(nbz, nby, nbx, 3, 3)
+    d = 10.0 ** rng.uniform(-2.0, np.log10(5.0), size=(nz, ny, nx, 3))
+    iz, iy, ix = np.meshgrid(np.arange(nz) // block, np.arange(ny) // block, np.arange(nx) // block, indexing="ij")
+    R = Rs[iz, iy, ix]
+    s = np.einsum("zyxij,zyxj,zyxkj->zyxik", R, d, R)
+    return 0.5 * (s + np.swapaxes(s, -1, -2))  # exactly symmetric
+
+
+def _c4_sigma(rng, cfg):
+    """c4 (homogeneous stand-in): a 2 m slab through the origin with normal (sin30,0,cos30),
+    TI sigma_h=0.02, sigma_v=0.005 about the normal (App. C, theta=30 deg, phi=0), in a
+    sigma_b host; then 20 ellipsoids: centre U over the grid inset 2 m, semi-axes U[0.5,2] m,
+    Haar rotation, eigenvalues sigma_b*10^U[-1,1]; later objects overwrite earlier ones."""
+    nx, ny, nz = cfg.n
+    s = np.zeros((nz, ny, nx, 3, 3))
+    s[...] = cfg.sigma_b * np.eye(3)
+    z, y, x = (cfg.cell_centers(2), cfg.cell_centers(1), cfg.cell_centers(0))
+    Z, Y, X = np.meshgrid(z, y, x, indexing="ij")
+    nrm = np.array([np.sin(np.radians(30)), 0.0, np.cos(np.radians(30))])
+    dist = X * nrm[0] + Y * nrm[1] + Z * nrm[2]
+    slab = np.abs(dist) <= 1.0
+    s[slab] = vti_tensor(0.02, 0.005, np.radians(30.0), 0.0)
+    lo = np.array([x[0], y[0], z[0]]) + 2.0
+    hi = np.array([x[-1], y[-1], z[-1]]) - 2.0
+    for _ in range(20):
+        c = rng.uniform(lo, hi)
+        ax = rng.uniform(0.5, 2.0, size=3)
+        R = haar_rotation(rng)
+        ev = cfg.sigma_b * 10.0 ** rng.uniform(-1.0, 1.0, size=3)
+        P = np.stack([X - c[0], Y - c[1], Z - c[2]], axis=-1) @ R  # body-frame coordinates
+        inside = np.sum((P / ax) ** 2, axis=-1) <= 1.0
+        s[inside] = R @ np.diag(ev) @ R.T
+    return s
+
+
+def _c5_sigma(rng, cfg, corr_len=2.0, spread=0.3, block=10):
+    """c5: three Gaussian random fields (correlation length 2 m); log10 d_i = log10 sigma_b +
+    spread * z_i clipped to [-2, 1]; one Haar rotation per block^3 cells (x-fastest);
+    sigma = R diag(d) R^T."""
+    nx, ny, nz = cfg.n
+    zf = [gaussian_random_field(rng, (nz, ny, nx), cfg.h, corr_len) for _ in range(3)]
+    d = np.stack([10.0 ** np.clip(np.log10(cfg.sigma_b) + spread * f, -2.0, 1.0) for f in zf], axis=-1)
+    nbx, nby, nbz = -(-nx // block), -(-ny // block), -(-nz // block)
+    Rs = np.stack([haar_rotation(rng) for _ in range(nbx * nby * nbz)]).reshape(nbz, nby, nbx, 3, 3)
+    iz, iy, ix = np.meshgrid(np.arange(nz) // block, np.arange(ny) // block, np.arange(nx) // block, indexing="ij")
+    R = Rs[iz, iy, ix]
+    s = np.einsum("zyxij,zyxj,zyxkj->zyxik", R, d, R)
+    return 0.5 * (s + np.swapaxes(s, -1, -2))  # exactly symmetric
+
+
+# ------------------------------------------------------------------------- c4 stations
+
+def c4_stations(n_stations=64, incl=70.0, azim=45.0, spacings=(1.0, 3.0, 7.0)):
+    """Trajectory through the origin, inclination 70 deg, azimuth 45 deg; station s at
+    t_s = -3.5 + (s - 31.5) * 0.5 m along d; receivers at Tx + {1,3,7} d; triaxial dipoles
+    along the tool axes x', y', z'.  Returns list of dict(tx, moments(3x3), rx(3x3))."""
+    F = tool_frame(incl, azim)
+    d = F[2]
+    out = []
+    for s in range(n_stations):
+        t = -3.5 + (s - 31.5) * 0.5
+        tx = t * d
+        out.append(dict(tx=tx, moments=F.copy(), rx=np.stack([tx + L * d for L in spacings])))
+    return out
+
+
+# ---------------------------------------------------------------------------- registry
+
+def make_config(name):
+    zdip = np.array([0.0, 0.0, 1.0])
+    tri = np.eye(3)
+    if name == "c1":
+        return Config("c1", (8, 8, 8), 0.25, 1.0, 1e5, 1, _c1_sigma,
+                      sources=[(np.array([0.0, 0.0, 1.0]), zdip)], receivers=[np.array([0.0, 0.0, 2.0])],
+                      boxes=[(0, 8, 0, 8, 0, 8)], restart=30, outer_tol=1e-10, parity_tol=1e-10)
+    if name in ("c2", "c2capped"):
+        log_hi = 1.0 if name == "c2" else 0.0
+        return Config(name, (32, 32, 32), 0.1, 0.1, 2e6, 2, lambda rng, c: _blocks_vti(rng, c, 8, log_hi),
+                      sources=[(np.zeros(3), zdip)],
+                      receivers=[np.array([0.0, 0.0, 0.5]), np.array([0.0, 0.0, 1.0])],
+                      boxes=[(0, 32, 0, 32, 0, 16), (0, 32, 0, 32, 16, 32)], restart=30, outer_tol=1e-8)
+    if name == "c2mini":
+        return Config(name, (8, 8, 8), 0.1, 0.1, 2e6, 2, lambda rng, c: _blocks_vti(rng, c, 2, 0.0),
+                      sources=[(np.zeros(3), zdip)], receivers=[np.array([0.0, 0.0, 0.5])],
+                      boxes=[(0, 8, 0, 8, 0, 4), (0, 8, 0, 8, 4, 8)], restart=30, outer_tol=1e-9)
+    if name == "c3h":
+        return Config(name, (64, 64, 64), 0.25, 1.0, 4e5, 3, _c3_sigma,
+                      sources=[(np.zeros(3), tri[i]) for i in range(3)],
+                      receivers=[np.array([0.0, 0.0, z]) for z in (1.0, 3.0, 7.0)],
+                      boxes=box_grid((64, 64, 64), (2, 2, 1)), restart=30, outer_tol=1e-8,
+                      note="homogeneous stand-in for the layered c3 (sigma_b = 1 S/m)")
+    if name == "c3mini":
+        return Config(name, (8, 8, 8), 0.25, 1.0, 4e5, 3, lambda rng, c: _c3_sigma(rng, c, 4),
+                      sources=[(np.zeros(3), tri[i]) for i in range(3)],
+                      receivers=[np.array([0.0, 0.0, 1.0])],
+                      boxes=box_grid((8, 8, 8), (2, 2, 1)), restart=30, outer_tol=1e-9)
+    if name == "c4h":
+        st = c4_stations()
+        return Config(name, (128, 128, 64), 0.25, 1.0, 4e5, 4, _c4_sigma,
+                      sources=[(st[31]["tx"], st[31]["moments"][i]) for i in range(3)],
+                      receivers=list(st[31]["rx"]),
+                      boxes=box_grid((128, 128, 64), (4, 2, 1)), restart=30, outer_tol=1e-6,
+                      note="homogeneous stand-in for the layered c4 (sigma_b = 1 S/m, 400 kHz)")
+    if name == "c5":
+        return Config(name, (256, 256, 128), 0.2, 0.5, 1e5, 5, _c5_sigma,
+                      sources=[(np.zeros(3), zdip)],
+                      receivers=[np.array([0.0, 0.0, 1.0]), np.array([0.0, 0.0, 3.0])],
+                      boxes=box_grid((256, 256, 128), (4, 4, 1)), restart=50, outer_tol=1e-6)
+    if name == "c5mini":
+        return Config(name, (8, 8, 8), 0.2, 0.5, 1e5, 5, lambda rng, c: _c5_sigma(rng, c, corr_len=0.4, block=2),
+                      sources=[(np.zeros(3), zdip)], receivers=[np.array([0.0, 0.0, 1.0])],
+                      boxes=box_grid((8, 8, 8), (2, 2, 1)), restart=50, outer_tol=1e-9)
+    raise KeyError(name)
+
+
+CONFIG_NAMES = ("c1", "c2", "c2capped", "c2mini", "c3h", "c3mini", "c4h", "c5", "c5mini")

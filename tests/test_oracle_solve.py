@@ -1,0 +1,80 @@
+"""Pins of oracle/gmres.py: dense LU truth, special cases, Born limit."""
+
+import numpy as np
+import pytest
+
+from ie_workloads import make_config
+from oracle import physics, operator as op
+from oracle.gmres import gmres
+
+
+def _setup(name):
+    cfg = make_config(name)
+    k0 = physics.wavenumber(cfg.sigma_b, cfg.freq)
+    ds = physics.contrast(cfg.sigma(), cfg.sigma_b)
+    pts = physics.centroids(cfg.n, cfg.hvec, cfg.origin)
+    E0 = np.stack([np.moveaxis(physics.incident_E(pts, s, m, k0, cfg.freq), -1, 0) for s, m in cfg.sources])
+    return cfg, k0, ds, E0
+
+
+class _Dense:
+    def __init__(self, M):
+        self.M = M
+
+    def __call__(self, x):
+        return (self.M @ x.ravel()).reshape(x.shape)
+
+
+def test_gmres_identity_one_iteration():
+    b = np.arange(12, dtype=complex).reshape(3, 2, 2, 1) + 1j
+    x, info = gmres(lambda v: v, b, tol=1e-12)
+    assert info["iters"] == 1 and info["converged"]
+    assert np.abs(x - b).max() < 1e-14
+
+
+def test_gmres_random_dense_system_vs_lu():
+    rng = np.random.default_rng(4)
+    n = 60
+    M = rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))
+    M = M / np.sqrt(n) * 0.5 + np.eye(n) * 2.0
+    b = rng.standard_normal(n) + 1j * rng.standard_normal(n)
+    for restart in (5, 30, 80):
+        x, info = gmres(_Dense(M), b, tol=1e-12, restart=restart)
+        assert info["converged"]
+        xs = np.linalg.solve(M, b)
+        assert np.linalg.norm(x - xs) / np.linalg.norm(xs) < 1e-10
+        assert info["relres_true"] <= 1e-12
+
+
+def test_c1_gmres_matches_dense_lu():
+    cfg, k0, ds, E0 = _setup("c1")
+    A = op.dense_matrix(cfg.n, cfg.hvec, k0, cfg.sigma_b, ds)
+    x_lu = np.linalg.solve(A, E0[0].ravel()).reshape(E0[0].shape)
+    Op = op.Operator(cfg.n, cfg.hvec, k0, cfg.sigma_b, ds)
+    x, info = gmres(Op, E0[0], x0=E0[0], tol=1e-10, restart=30)
+    assert info["converged"] and info["relres_true"] <= 1e-10
+    assert np.linalg.norm(x - x_lu) / np.linalg.norm(x_lu) < 1e-9
+    # the discrete system is well conditioned (SURVEY 8c-6 reports cond ~ 5.9)
+    assert np.linalg.cond(A) < 20
+
+
+def test_zero_contrast_returns_incident_in_zero_iterations():
+    cfg, k0, ds, E0 = _setup("c1")
+    Op = op.Operator(cfg.n, cfg.hvec, k0, cfg.sigma_b, np.zeros_like(ds))
+    x, info = gmres(Op, E0[0], x0=E0[0], tol=1e-12)
+    assert info["iters"] == 0 and info["converged"]
+    assert np.array_equal(x, E0[0])
+
+
+def test_born_limit_second_order():
+    """E(eps dsigma) = E0 + eps G dsigma E0 + O(eps^2): the remainder falls 100x per decade."""
+    cfg, k0, ds, E0 = _setup("c1")
+    rem = []
+    for eps in (1e-2, 1e-3):
+        A = op.dense_matrix(cfg.n, cfg.hvec, k0, cfg.sigma_b, eps * ds)
+        E = np.linalg.solve(A, E0[0].ravel()).reshape(E0[0].shape)
+        Op = op.Operator(cfg.n, cfg.hvec, k0, cfg.sigma_b, eps * ds)
+        born = E0[0] + Op.scatter(E0[0])
+        rem.append(np.linalg.norm(E - born))
+    ratio = rem[0] / rem[1]
+    assert 80 < ratio < 125
