@@ -47,15 +47,19 @@ def direct_rows(n, h, k0, sigma_b, dsigma, E, cells, identity=True):
     nx, ny, nz = n
     dv = h[0] * h[1] * h[2]
     J = contrast_source(dsigma, E)  # (3, nz, ny, nx)
-    iz, iy, ix = np.meshgrid(np.arange(nz), np.arange(ny), np.arange(nx), indexing="ij")
     out = np.zeros((len(cells), 3), np.complex128)
+    slab = max(1, (1 << 20) // (nx * ny))  # sum over z-slabs to bound memory on large grids
     for t, (cx, cy, cz) in enumerate(cells):
-        Rv = np.stack([(cx - ix) * h[0], (cy - iy) * h[1], (cz - iz) * h[2]], axis=-1)
-        zero = (ix == cx) & (iy == cy) & (iz == cz)
-        Rv_safe = np.where(zero[..., None], 1.0, Rv)
-        K = physics.green_E(Rv_safe, k0, sigma_b) * dv
-        K[zero] = physics.self_term(k0, sigma_b, dv)
-        s = np.einsum("zyxpq,qzyx->p", K, J)
+        s = np.zeros(3, np.complex128)
+        for z0 in range(0, nz, slab):
+            z1 = min(nz, z0 + slab)
+            iz, iy, ix = np.meshgrid(np.arange(z0, z1), np.arange(ny), np.arange(nx), indexing="ij")
+            Rv = np.stack([(cx - ix) * h[0], (cy - iy) * h[1], (cz - iz) * h[2]], axis=-1)
+            zero = (ix == cx) & (iy == cy) & (iz == cz)
+            Rv_safe = np.where(zero[..., None], 1.0, Rv)
+            K = physics.green_E(Rv_safe, k0, sigma_b) * dv
+            K[zero] = physics.self_term(k0, sigma_b, dv)
+            s += np.einsum("zyxpq,qzyx->p", K, J[:, z0:z1])
         out[t] = (E[:, cz, cy, cx] if identity else 0.0) - s
     return out
 

@@ -1,0 +1,612 @@
+// C-ABI entry points (include/ie_b200.h) and the domain-decomposition orchestrator
+// (Algorithm 1; Eqs. 19-24).
+#include <math.h>
+
+#include <algorithm>
+#include <complex>
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "ie_internal.h"
+
+static thread_local std::string g_err;  // errors without a context (ie_create)
+
+namespace ie {
+
+ie_status fail(ie_ctx* c, ie_status s, const std::string& msg) {
+  if (c) c->err = msg;
+  g_err = msg;
+  return s;
+}
+ie_status cuda_fail(ie_ctx* c, cudaError_t e, const char* where) {
+  std::string m = std::string("CUDA error in ") + where + ": " + cudaGetErrorString(e);
+  cudaGetLastError();  // clear sticky-free errors
+  return fail(c, e == cudaErrorMemoryAllocation ? IE_ERR_OUT_OF_MEMORY : IE_ERR_CUDA, m);
+}
+
+static long long ncell(const ie_ctx* c) { return (long long)c->g.nx * c->g.ny * c->g.nz; }
+
+static bool box_ok(const ie_ctx* c, const ie_box& b, std::string* why) {
+  if (b.i0 < 0 || b.j0 < 0 || b.k0 < 0 || b.i1 > c->g.nx || b.j1 > c->g.ny || b.k1 > c->g.nz || b.i1 <= b.i0 ||
+      b.j1 <= b.j0 || b.k1 <= b.k0) {
+    *why = "box outside the grid or empty";
+    return false;
+  }
+  if (!is_pow2(b.i1 - b.i0) || !is_pow2(b.j1 - b.j0) || !is_pow2(b.k1 - b.k0)) {
+    *why = "box extents must be powers of two";
+    return false;
+  }
+  return true;
+}
+
+static ie_box full_box(const ie_ctx* c) { return ie_box{0, c->g.nx, 0, c->g.ny, 0, c->g.nz}; }
+
+static const double* dsig_at(const ie_ctx* c, const ie_box& b) {
+  return c->dsig + ((long long)b.k0 * c->g.ny + b.j0) * c->g.nx + b.i0;
+}
+
+// Apply on a box-shaped domain for nitems inputs (x[i] compact over the source sub-box src,
+// which is relative to the domain box).  y = alpha x + beta G dsigma x (+ y).
+static ie_status apply_many(ie_ctx* c, Arena& ar, const ie_box& dom, const ie_box& src,
+                            const std::vector<const double2*>& x, const std::vector<double2*>& y, double alpha,
+                            double beta, int acc) {
+  const int bx = dom.i1 - dom.i0, by = dom.j1 - dom.j0, bz = dom.k1 - dom.k0;
+  ie_status st;
+  const GreenSpec* gs = green_for(c, bx, by, bz, &st);
+  if (!gs) return st;
+  const int n = (int)x.size();
+  const int items = std::min(n, kMaxItems);
+  const size_t mark = ar.used;
+  double2* scratch = (double2*)ar.take(apply_scratch_bytes(bx, by, bz, items));
+  if (!scratch) {
+    ar.used = mark;
+    return fail(c, IE_ERR_OUT_OF_MEMORY, "workspace too small for the operator (need " + std::to_string(ar.peak) +
+                                             " bytes; see ie_workspace_query)");
+  }
+  ApplyParams p;
+  p.nx = bx;
+  p.ny = by;
+  p.nz = bz;
+  p.ds_cs = ncell(c);
+  p.ds_zs = (long long)c->g.nx * c->g.ny;
+  p.ds_ys = c->g.nx;
+  p.ghat = gs->oct;
+  p.X1 = scratch;
+  p.X2 = scratch + (size_t)items * 3 * 2 * bx * by * bz;
+  p.alpha = alpha;
+  p.beta = beta;
+  p.accumulate = acc;
+  for (int b0 = 0; b0 < n; b0 += kMaxItems) {
+    const int nb = std::min(kMaxItems, n - b0);
+    p.n_items = nb;
+    for (int i = 0; i < nb; ++i) {
+      ApplyItem& it = p.items[i];
+      it.x = x[b0 + i];
+      it.y = y[b0 + i];
+      it.dsig = dsig_at(c, dom);
+      it.xscale = 1.0;
+      it.sx0 = src.i0;
+      it.sx1 = src.i1;
+      it.sy0 = src.j0;
+      it.sy1 = src.j1;
+      it.sz0 = src.k0;
+      it.sz1 = src.k1;
+    }
+    st = launch_apply(c, p);
+    if (st) break;
+  }
+  ar.used = mark;
+  return st;
+}
+
+static Arena arena_of(ie_ctx* c) {
+  Arena a;
+  a.base = c->ws;
+  a.cap = c->ws_bytes;
+  return a;
+}
+
+static size_t dd_bytes(int nx, int ny, int nz, const ie_box* boxes, int n_boxes, int ns, int m) {
+  const size_t len = 3ull * nx * ny * nz;
+  size_t fixed = 2 * (size_t)ns * len * sizeof(double2) + 3 * (size_t)ns * len * sizeof(double2) + 8192;
+  // largest same-shape group (Jacobi batch) and any single box (GS)
+  std::map<std::vector<int>, int> groups;
+  for (int i = 0; i < n_boxes; ++i)
+    groups[{boxes[i].i1 - boxes[i].i0, boxes[i].j1 - boxes[i].j0, boxes[i].k1 - boxes[i].k0}]++;
+  size_t var = apply_scratch_bytes(nx, ny, nz, std::min(ns, kMaxItems));
+  for (auto& g : groups) {
+    const int bx = g.first[0], by = g.first[1], bz = g.first[2];
+    var = std::max(var, gmres_scratch_bytes(bx, by, bz, g.second * ns, m));
+    var = std::max(var, apply_scratch_bytes(bx, by, bz, std::min(g.second * ns, kMaxItems)));
+  }
+  return fixed + var + 4096;
+}
+
+}  // namespace ie
+
+using namespace ie;
+
+extern "C" {
+
+const char* ie_last_error(const ie_ctx* c) { return c ? c->err.c_str() : g_err.c_str(); }
+
+ie_status ie_create(const ie_grid* g, const ie_background* bg, double freq_hz, void* stream, ie_ctx** out) {
+  if (!out) return fail(nullptr, IE_ERR_INVALID_ARGUMENT, "out is NULL");
+  *out = nullptr;
+  if (!g || !bg) return fail(nullptr, IE_ERR_INVALID_ARGUMENT, "grid or background is NULL");
+  const int n[3] = {g->nx, g->ny, g->nz};
+  for (int a = 0; a < 3; ++a)
+    if (!is_pow2(n[a]) || n[a] > 512)
+      return fail(nullptr, IE_ERR_INVALID_ARGUMENT, "grid dimensions must be powers of two in [1, 512]");
+  if (!(g->dx > 0) || !(g->dy > 0) || !(g->dz > 0)) return fail(nullptr, IE_ERR_INVALID_ARGUMENT, "cell sizes must be > 0");
+  if (!(freq_hz > 0) || !std::isfinite(freq_hz)) return fail(nullptr, IE_ERR_INVALID_ARGUMENT, "frequency must be > 0");
+  if (bg->n_layers != 1 || bg->table)
+    return fail(nullptr, IE_ERR_UNSUPPORTED, "layered backgrounds (SURVEY 8(a) A3L) are not built yet; use n_layers = 1");
+  if (!bg->sigma || !(bg->sigma[0] > 0) || !std::isfinite(bg->sigma[0]))
+    return fail(nullptr, IE_ERR_INVALID_ARGUMENT, "background conductivity must be > 0");
+  ie_ctx* c = new ie_ctx();
+  c->g = *g;
+  c->sigma_b = bg->sigma[0];
+  c->freq = freq_hz;
+  c->omega = 2 * kPi * freq_hz;
+  c->stream = (cudaStream_t)stream;
+  // k0 = sqrt(i omega mu0 sigma0), Re, Im > 0 (Eq. 7)
+  c->k0 = std::sqrt(cplx(0.0, c->omega * kMu0 * c->sigma_b));
+  // self term K(0) = (1/sigma0)[(2/3)(1 - i k0 a) e^{i k0 a} - 1]  (reading R3)
+  const double dv = g->dx * g->dy * g->dz;
+  const double a = cbrt(3.0 * dv / (4.0 * kPi));
+  const cplx ika = cplx(0.0, 1.0) * c->k0 * a;
+  c->self = ((2.0 / 3.0) * (1.0 - ika) * std::exp(ika) - 1.0) / c->sigma_b;
+  int dev_count = 0;
+  cudaError_t e = cudaGetDeviceCount(&dev_count);
+  if (e != cudaSuccess || dev_count == 0) {
+    delete c;
+    return fail(nullptr, IE_ERR_CUDA, "no CUDA device available (this library has no CPU fallback)");
+  }
+  ie_status st = build_twiddles(c);
+  if (!st) {
+    GreenSpec gs;
+    st = build_green(c, g->nx, g->ny, g->nz, &gs);
+    if (!st) c->greens.push_back(gs);
+  }
+  if (st) {
+    g_err = c->err;
+    ie_destroy(c);
+    return st;
+  }
+  *out = c;
+  return IE_OK;
+}
+
+ie_status ie_destroy(ie_ctx* c) {
+  if (!c) return IE_OK;
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  else cudaDeviceSynchronize();
+  for (auto& g : c->greens) cudaFree(g.oct);
+  cudaFree(c->dsig);
+  cudaFree(c->e0);
+  cudaFree(c->tw.dev);
+  cudaFree(c->d_red);
+  if (c->h_red) cudaFreeHost(c->h_red);
+  delete c;
+  return IE_OK;
+}
+
+ie_status ie_workspace_query(ie_ctx* c, const ie_box* boxes, int32_t n_boxes, int32_t nrhs, int32_t restart,
+                             size_t* bytes) {
+  if (!c || !bytes || nrhs < 1 || restart < 1 || restart > 128 || n_boxes < 0 || (n_boxes > 0 && !boxes))
+    return fail(c, IE_ERR_INVALID_ARGUMENT, "workspace_query: bad arguments");
+  const int nx = c->g.nx, ny = c->g.ny, nz = c->g.nz;
+  size_t b = apply_scratch_bytes(nx, ny, nz, std::min(nrhs, kMaxItems));
+  b = std::max(b, gmres_scratch_bytes(nx, ny, nz, nrhs, restart));
+  if (n_boxes > 0) b = std::max(b, dd_bytes(nx, ny, nz, boxes, n_boxes, nrhs, restart));
+  b = std::max(b, (size_t)(296 + 64 * nrhs) * 3 * sizeof(double2));
+  *bytes = b + 65536;
+  return IE_OK;
+}
+
+ie_status ie_bind_workspace(ie_ctx* c, void* dptr, size_t bytes) {
+  if (!c || (!dptr && bytes)) return fail(c, IE_ERR_INVALID_ARGUMENT, "bind_workspace: bad arguments");
+  if (((uintptr_t)dptr) & 255) return fail(c, IE_ERR_INVALID_ARGUMENT, "workspace must be 256-byte aligned");
+  c->ws = (char*)dptr;
+  c->ws_bytes = bytes;
+  return IE_OK;
+}
+
+ie_status ie_set_contrast(ie_ctx* c, const void* sigma_dev, int32_t layout) {
+  if (!c || !sigma_dev || (layout != 0 && layout != 1))
+    return fail(c, IE_ERR_INVALID_ARGUMENT, "set_contrast: bad arguments (layout 0 = FULL9, 1 = SYM6)");
+  return pack_contrast(c, sigma_dev, layout);
+}
+
+ie_status ie_set_source(ie_ctx* c, int32_t n_src, const double* pos, const double* moment) {
+  if (!c || n_src < 1 || !pos || !moment) return fail(c, IE_ERR_INVALID_ARGUMENT, "set_source: bad arguments");
+  const long long N = ncell(c);
+  if (c->e0 && c->n_src != n_src) {
+    cudaFree(c->e0);
+    c->e0 = nullptr;
+  }
+  if (!c->e0) IE_CUDA(c, cudaMalloc(&c->e0, (size_t)n_src * 3 * N * sizeof(double2)));
+  c->n_src = n_src;
+  ie_status st = compute_incident(c, n_src, pos, moment, c->e0);
+  if (st) {
+    c->n_src = 0;
+    return st;
+  }
+  // remember sources for H0 at the receivers
+  c->err.clear();
+  c->src_pos.assign(pos, pos + 3 * n_src);
+  c->src_mom.assign(moment, moment + 3 * n_src);
+  return IE_OK;
+}
+
+ie_status ie_get_incident(ie_ctx* c, void* e0_dev) {
+  if (!c || !e0_dev) return fail(c, IE_ERR_INVALID_ARGUMENT, "get_incident: bad arguments");
+  if (!c->e0 || c->n_src == 0) return fail(c, IE_ERR_STATE, "no sources set");
+  IE_CUDA(c, cudaMemcpyAsync(e0_dev, c->e0, (size_t)c->n_src * 3 * ncell(c) * sizeof(double2),
+                             cudaMemcpyDeviceToDevice, c->stream));
+  return IE_OK;
+}
+
+ie_status ie_set_incident(ie_ctx* c, int32_t n_src, const void* e0_dev) {
+  if (!c || n_src < 1 || !e0_dev) return fail(c, IE_ERR_INVALID_ARGUMENT, "set_incident: bad arguments");
+  const long long N = ncell(c);
+  if (c->e0 && c->n_src != n_src) {
+    cudaFree(c->e0);
+    c->e0 = nullptr;
+  }
+  if (!c->e0) IE_CUDA(c, cudaMalloc(&c->e0, (size_t)n_src * 3 * N * sizeof(double2)));
+  IE_CUDA(c, cudaMemcpyAsync(c->e0, e0_dev, (size_t)n_src * 3 * N * sizeof(double2), cudaMemcpyDeviceToDevice,
+                             c->stream));
+  c->n_src = n_src;
+  c->src_pos.clear();
+  c->src_mom.clear();
+  return IE_OK;
+}
+
+ie_status ie_apply_operator(ie_ctx* c, const ie_box* box, int32_t nrhs, const void* x_dev, void* y_dev) {
+  if (!c || nrhs < 1 || !x_dev || !y_dev || x_dev == y_dev)
+    return fail(c, IE_ERR_INVALID_ARGUMENT, "apply_operator: bad arguments");
+  if (!c->contrast_set) return fail(c, IE_ERR_STATE, "apply_operator before set_contrast");
+  const ie_box b = box ? *box : full_box(c);
+  std::string why;
+  if (!box_ok(c, b, &why)) return fail(c, IE_ERR_INVALID_ARGUMENT, why);
+  const long long nb = 3LL * (b.i1 - b.i0) * (b.j1 - b.j0) * (b.k1 - b.k0);
+  std::vector<const double2*> x;
+  std::vector<double2*> y;
+  for (int r = 0; r < nrhs; ++r) {
+    x.push_back((const double2*)x_dev + r * nb);
+    y.push_back((double2*)y_dev + r * nb);
+  }
+  Arena ar = arena_of(c);
+  const ie_box src{0, b.i1 - b.i0, 0, b.j1 - b.j0, 0, b.k1 - b.k0};
+  return apply_many(c, ar, b, src, x, y, 1.0, -1.0, 0);
+}
+
+ie_status ie_solve_subdomain(ie_ctx* c, const ie_box* box, int32_t nrhs, const void* b_dev, void* x_dev,
+                             const ie_gmres_opts* o, ie_solve_stats* stats) {
+  if (!c || nrhs < 1 || !b_dev || !x_dev || !o || !stats || o->restart < 1 || o->restart > 128 || !(o->tol > 0))
+    return fail(c, IE_ERR_INVALID_ARGUMENT, "solve_subdomain: bad arguments");
+  if (!c->contrast_set) return fail(c, IE_ERR_STATE, "solve before set_contrast");
+  const ie_box b = box ? *box : full_box(c);
+  std::string why;
+  if (!box_ok(c, b, &why)) return fail(c, IE_ERR_INVALID_ARGUMENT, why);
+  const int bx = b.i1 - b.i0, by = b.j1 - b.j0, bz = b.k1 - b.k0;
+  const long long nb = 3LL * bx * by * bz;
+  std::vector<GmresSystem> sys;
+  for (int r = 0; r < nrhs; ++r)
+    sys.push_back(GmresSystem{(const double2*)b_dev + r * nb, (double2*)x_dev + r * nb, dsig_at(c, b), o->tol,
+                              o->min_iters});
+  Arena ar = arena_of(c);
+  std::vector<GmresResult> res;
+  ie_status st = gmres_batched(c, ar, bx, by, bz, (long long)c->g.nx * c->g.ny, c->g.nx, sys, o->restart,
+                               o->max_iters, res, nullptr);
+  if (st) return st;
+  IE_CUDA(c, cudaStreamSynchronize(c->stream));
+  bool allc = true, brk = false;
+  for (int r = 0; r < nrhs; ++r) {
+    stats[r].iters = res[r].iters;
+    stats[r].restarts = res[r].restarts;
+    stats[r].converged = res[r].converged;
+    stats[r].relres_est = res[r].relres_est;
+    stats[r].relres_true = res[r].relres_true;
+    allc = allc && res[r].converged;
+    brk = brk || res[r].breakdown;
+  }
+  if (brk) return fail(c, IE_ERR_BREAKDOWN, "non-finite values in GMRES");
+  if (!allc) return fail(c, IE_ERR_NOT_CONVERGED, "GMRES reached max_iters");
+  return IE_OK;
+}
+
+// ------------------------------------------------------------------------ Algorithm 1
+ie_status ie_solve_dd(ie_ctx* c, const ie_dd_opts* o, void* e_dev, int32_t init_from_e, ie_dd_stats* stats) {
+  if (!c || !o || !e_dev || !stats) return fail(c, IE_ERR_INVALID_ARGUMENT, "solve_dd: bad arguments");
+  if (!c->contrast_set || !c->e0 || c->n_src < 1) return fail(c, IE_ERR_STATE, "solve_dd needs contrast and sources");
+  if (o->inner.restart < 1 || o->inner.restart > 128 || !(o->outer_tol > 0) || o->max_sweeps < 0)
+    return fail(c, IE_ERR_INVALID_ARGUMENT, "solve_dd: bad options");
+  const int ns = c->n_src;
+  const long long N = ncell(c), len = 3 * N;
+  double2* E = (double2*)e_dev;
+  const int m = o->inner.restart;
+  const ie_box fb = full_box(c);
+  stats->sweeps = 0;
+  stats->total_inner_iters = 0;
+  stats->full_applies = 0;
+  stats->sub_applies = 0;
+  stats->e_final = 0;
+  if (!init_from_e) IE_CUDA(c, cudaMemcpyAsync(E, c->e0, (size_t)ns * len * sizeof(double2), cudaMemcpyDeviceToDevice, c->stream));
+  Arena ar = arena_of(c);
+
+  if (o->scheme == IE_DD_FULL) {
+    std::vector<GmresSystem> sys;
+    for (int r = 0; r < ns; ++r)
+      sys.push_back(GmresSystem{c->e0 + r * len, E + r * len, c->dsig, o->outer_tol, o->inner.min_iters});
+    std::vector<GmresResult> res;
+    long long ap = 0;
+    ie_status st = gmres_batched(c, ar, c->g.nx, c->g.ny, c->g.nz, (long long)c->g.nx * c->g.ny, c->g.nx, sys, m,
+                                 o->inner.max_iters, res, &ap);
+    if (st) return st;
+    bool allc = true, brk = false;
+    for (int r = 0; r < ns; ++r) {
+      stats->total_inner_iters += res[r].iters;
+      stats->e_final = std::max(stats->e_final, res[r].relres_true);
+      if (stats->e_hist) stats->e_hist[r] = res[r].relres_true;
+      allc = allc && res[r].converged;
+      brk = brk || res[r].breakdown;
+    }
+    stats->full_applies = (int)ap;
+    if (brk) return fail(c, IE_ERR_BREAKDOWN, "non-finite values in GMRES");
+    if (!allc) return fail(c, IE_ERR_NOT_CONVERGED, "full-domain GMRES reached max_iters");
+    return IE_OK;
+  }
+  if (o->scheme != IE_DD_JACOBI && o->scheme != IE_DD_GAUSS_SEIDEL)
+    return fail(c, IE_ERR_INVALID_ARGUMENT, "solve_dd: unknown scheme");
+  const int M = o->n_boxes;
+  if (M < 1 || !o->boxes) return fail(c, IE_ERR_INVALID_ARGUMENT, "solve_dd: no boxes");
+  // partition check (Eq. 11): non-overlapping cover of the grid
+  {
+    std::vector<unsigned char> cover(N, 0);
+    for (int i = 0; i < M; ++i) {
+      std::string why;
+      if (!box_ok(c, o->boxes[i], &why)) return fail(c, IE_ERR_INVALID_ARGUMENT, "box " + std::to_string(i) + ": " + why);
+      const ie_box& b = o->boxes[i];
+      for (int k = b.k0; k < b.k1; ++k)
+        for (int j = b.j0; j < b.j1; ++j)
+          for (int x = b.i0; x < b.i1; ++x) cover[((long long)k * c->g.ny + j) * c->g.nx + x]++;
+    }
+    for (long long i = 0; i < N; ++i)
+      if (cover[i] != 1) return fail(c, IE_ERR_INVALID_ARGUMENT, "boxes must partition the grid (Eq. 11)");
+  }
+  // persistent DD buffers
+  double2* S = (double2*)ar.take((size_t)ns * len * sizeof(double2));  // coupling field G dsigma E
+  double2* T = (double2*)ar.take((size_t)ns * len * sizeof(double2));  // E0 + S
+  double2* Bb = (double2*)ar.take((size_t)ns * len * sizeof(double2)); // per-box rhs   [box][rhs][3Nb]
+  double2* Xb = (double2*)ar.take((size_t)ns * len * sizeof(double2)); // per-box x
+  double2* Ob = (double2*)ar.take((size_t)ns * len * sizeof(double2)); // per-box old x / delta
+  if (!S || !T || !Bb || !Xb || !Ob)
+    return fail(c, IE_ERR_OUT_OF_MEMORY, "workspace too small for DD (see ie_workspace_query with the boxes)");
+  std::vector<long long> boff(M);  // offset of box i's [rhs][3Nb] block
+  {
+    long long off = 0;
+    for (int i = 0; i < M; ++i) {
+      boff[i] = off;
+      const ie_box& b = o->boxes[i];
+      off += (long long)ns * 3 * (b.i1 - b.i0) * (b.j1 - b.j0) * (b.k1 - b.k0);
+    }
+  }
+  auto nbox = [&](int i) {
+    const ie_box& b = o->boxes[i];
+    return 3LL * (b.i1 - b.i0) * (b.j1 - b.j0) * (b.k1 - b.k0);
+  };
+  std::vector<double> e0n(ns), e(ns), eprev(ns);
+  std::vector<int> grow(ns, 0);
+  std::vector<char> active(ns, 1);
+  ie_status st = norms2(c, c->e0, nullptr, ns, len, len, e0n.data());
+  if (st) return st;
+  for (int r = 0; r < ns; ++r) e0n[r] = sqrt(e0n[r]);
+
+  auto full_G = [&](const std::vector<int>& rr) -> ie_status {  // S_r = G dsigma E_r
+    std::vector<const double2*> x;
+    std::vector<double2*> y;
+    for (int r : rr) {
+      x.push_back(E + r * len);
+      y.push_back(S + r * len);
+    }
+    stats->full_applies += (int)rr.size();
+    return apply_many(c, ar, fb, fb, x, y, 0.0, 1.0, 0);
+  };
+  auto residual = [&](const std::vector<int>& rr) -> ie_status {  // T = E0 + S; e = ||T - E|| / ||E0||
+    for (int r : rr) {
+      launch_axpby(c, T + r * len, 1.0, c->e0 + r * len, 1.0, S + r * len, len);
+      double v;
+      ie_status s2 = norms2(c, T + r * len, E + r * len, 1, len, 0, &v);
+      if (s2) return s2;
+      e[r] = e0n[r] > 0 ? sqrt(v) / e0n[r] : 0.0;
+    }
+    return IE_OK;
+  };
+  std::vector<int> all;
+  for (int r = 0; r < ns; ++r) all.push_back(r);
+  st = full_G(all);
+  if (st) return st;
+  st = residual(all);
+  if (st) return st;
+  for (int r = 0; r < ns; ++r) {
+    if (stats->e_hist) stats->e_hist[r] = e[r];
+    active[r] = e[r] > o->outer_tol;
+  }
+  bool diverged = false, breakdown = false;
+  // rhs b_i = T|_i - G_ii dsigma_i E|_i for boxes in `ids` and rhs in `rr`; x0 = E|_i
+  auto assemble = [&](const std::vector<int>& ids, const std::vector<int>& rr) -> ie_status {
+    for (int i : ids) {
+      const ie_box& b = o->boxes[i];
+      for (int r : rr) {
+        double2* bb = Bb + boff[i] + r * nbox(i);
+        double2* xb = Xb + boff[i] + r * nbox(i);
+        double2* ob = Ob + boff[i] + r * nbox(i);
+        launch_gather(c, T + r * len, bb, b, 1, 0, 0);
+        launch_gather(c, E + r * len, ob, b, 1, 0, 0);
+        launch_axpby(c, xb, 1.0, ob, 0.0, nullptr, nbox(i));
+      }
+      std::vector<const double2*> x;
+      std::vector<double2*> y;
+      for (int r : rr) {
+        x.push_back(Ob + boff[i] + r * nbox(i));
+        y.push_back(Bb + boff[i] + r * nbox(i));
+      }
+      const ie_box src{0, b.i1 - b.i0, 0, b.j1 - b.j0, 0, b.k1 - b.k0};
+      stats->sub_applies += (int)rr.size();
+      ie_status s2 = apply_many(c, ar, b, src, x, y, 0.0, -1.0, 1);
+      if (s2) return s2;
+    }
+    return IE_OK;
+  };
+  auto solve_boxes = [&](const std::vector<int>& ids, const std::vector<int>& rr, int sweep) -> ie_status {
+    // all boxes in ids share one shape
+    const ie_box& b0 = o->boxes[ids[0]];
+    std::vector<GmresSystem> sys;
+    std::vector<std::pair<int, int>> who;
+    for (int i : ids)
+      for (int r : rr) {
+        const double thr = o->adaptive ? e[r] * o->inner_tol_factor : o->inner_tol_fixed;
+        sys.push_back(GmresSystem{Bb + boff[i] + r * nbox(i), Xb + boff[i] + r * nbox(i), dsig_at(c, o->boxes[i]), thr,
+                                  std::max(1, o->inner.min_iters)});
+        who.push_back({i, r});
+      }
+    std::vector<GmresResult> res;
+    const size_t mark = ar.used;
+    long long ap = 0;
+    ie_status s2 = gmres_batched(c, ar, b0.i1 - b0.i0, b0.j1 - b0.j0, b0.k1 - b0.k0, (long long)c->g.nx * c->g.ny,
+                                 c->g.nx, sys, m, o->inner.max_iters, res, &ap);
+    ar.used = mark;
+    if (s2) return s2;
+    stats->sub_applies += (int)ap;
+    for (size_t t = 0; t < who.size(); ++t) {
+      stats->total_inner_iters += res[t].iters;
+      if (res[t].breakdown) breakdown = true;
+      if (stats->iters) stats->iters[((size_t)sweep * M + who[t].first) * ns + who[t].second] = res[t].iters;
+    }
+    return IE_OK;
+  };
+  // group boxes by shape (Jacobi batches)
+  std::map<std::vector<int>, std::vector<int>> groups;
+  for (int i = 0; i < M; ++i) {
+    const ie_box& b = o->boxes[i];
+    groups[{b.i1 - b.i0, b.j1 - b.j0, b.k1 - b.k0}].push_back(i);
+  }
+
+  int sweep = 0;
+  while (sweep < o->max_sweeps) {
+    std::vector<int> rr;
+    for (int r = 0; r < ns; ++r)
+      if (active[r]) rr.push_back(r);
+    if (rr.empty()) break;
+    if (o->scheme == IE_DD_JACOBI) {
+      for (auto& g : groups) {
+        st = assemble(g.second, rr);
+        if (st) return st;
+        st = solve_boxes(g.second, rr, sweep);
+        if (st) return st;
+      }
+      for (int i = 0; i < M; ++i)
+        for (int r : rr) launch_scatter(c, E + r * len, Xb + boff[i] + r * nbox(i), o->boxes[i], 1, 0, 0);
+      st = full_G(rr);
+      if (st) return st;
+    } else {  // Gauss-Seidel, boxes in the given order
+      for (int i = 0; i < M; ++i) {
+        for (int r : rr) launch_axpby(c, T + r * len, 1.0, c->e0 + r * len, 1.0, S + r * len, len);
+        st = assemble({i}, rr);
+        if (st) return st;
+        st = solve_boxes({i}, rr, sweep);
+        if (st) return st;
+        // delta = x_new - x_old on box i; S += G dsigma (delta restricted to box i)
+        std::vector<const double2*> x;
+        std::vector<double2*> y;
+        for (int r : rr) {
+          double2* ob = Ob + boff[i] + r * nbox(i);
+          launch_axpby(c, ob, 1.0, Xb + boff[i] + r * nbox(i), -1.0, ob, nbox(i));
+          x.push_back(ob);
+          y.push_back(S + r * len);
+          launch_scatter(c, E + r * len, Xb + boff[i] + r * nbox(i), o->boxes[i], 1, 0, 0);
+        }
+        stats->full_applies += (int)rr.size();
+        st = apply_many(c, ar, fb, o->boxes[i], x, y, 0.0, 1.0, 1);
+        if (st) return st;
+      }
+    }
+    ++sweep;
+    eprev = e;
+    st = residual(rr);
+    if (st) return st;
+    for (int r : rr) {
+      grow[r] = e[r] > eprev[r] ? grow[r] + 1 : 0;
+      if (!std::isfinite(e[r])) breakdown = true;
+      if (grow[r] >= 3) diverged = true;
+      active[r] = e[r] > o->outer_tol && std::isfinite(e[r]);
+    }
+    if (stats->e_hist)
+      for (int r = 0; r < ns; ++r) stats->e_hist[(size_t)sweep * ns + r] = e[r];
+    if (diverged || breakdown) break;
+  }
+  IE_CUDA(c, cudaStreamSynchronize(c->stream));
+  stats->sweeps = sweep;
+  bool allc = true;
+  for (int r = 0; r < ns; ++r) {
+    stats->e_final = std::max(stats->e_final, e[r]);
+    allc = allc && e[r] <= o->outer_tol;
+  }
+  if (breakdown) return fail(c, IE_ERR_BREAKDOWN, "non-finite values in the DD iteration");
+  if (!allc) return fail(c, IE_ERR_NOT_CONVERGED, diverged ? "DD residual grew for 3 sweeps" : "DD reached max_sweeps");
+  return IE_OK;
+}
+
+ie_status ie_receiver_fields(ie_ctx* c, const void* e_dev, int32_t n_rx, const double* rx_pos, void* h_host,
+                             void* v_host) {
+  if (!c || !e_dev || n_rx < 1 || !rx_pos || !h_host) return fail(c, IE_ERR_INVALID_ARGUMENT, "receiver_fields: bad arguments");
+  if (!c->contrast_set || c->n_src < 1) return fail(c, IE_ERR_STATE, "receiver_fields needs contrast and sources");
+  if ((int)c->src_pos.size() != 3 * c->n_src)
+    return fail(c, IE_ERR_STATE, "receiver_fields needs dipole sources (ie_set_source) for H0");
+  Arena ar = arena_of(c);
+  double2* scratch = (double2*)ar.take((size_t)(296 + c->n_src * n_rx) * 3 * sizeof(double2));
+  if (!scratch) return fail(c, IE_ERR_OUT_OF_MEMORY, "workspace too small for receivers");
+  std::vector<cplx> h((size_t)c->n_src * n_rx * 3);
+  ie_status st = receivers(c, (const double2*)e_dev, n_rx, rx_pos, h.data(), c->src_pos.data(), c->src_mom.data(),
+                           c->n_src, scratch);
+  if (st) return st;
+  std::memcpy(h_host, h.data(), h.size() * sizeof(cplx));
+  if (v_host) {
+    cplx* v = (cplx*)v_host;
+    const cplx iwm = cplx(0.0, c->omega * kMu0);
+    for (size_t i = 0; i < h.size(); ++i) v[i] = iwm * h[i];
+  }
+  return IE_OK;
+}
+
+ie_status ie_get_info(const ie_ctx* c, ie_info* info) {
+  if (!c || !info) return IE_ERR_INVALID_ARGUMENT;
+  info->k0_re = c->k0.real();
+  info->k0_im = c->k0.imag();
+  info->self_re = c->self.real();
+  info->self_im = c->self.imag();
+  info->n_src = c->n_src;
+  info->kernel_launches = (int32_t)std::min<long long>(c->launches, 0x7fffffff);
+  return IE_OK;
+}
+
+ie_status ie_get_green_octant(ie_ctx* c, const ie_box* box, void* host_out) {
+  if (!c || !host_out) return fail(c, IE_ERR_INVALID_ARGUMENT, "get_green_octant: bad arguments");
+  const ie_box b = box ? *box : full_box(c);
+  std::string why;
+  if (!box_ok(c, b, &why)) return fail(c, IE_ERR_INVALID_ARGUMENT, why);
+  ie_status st;
+  const GreenSpec* gs = green_for(c, b.i1 - b.i0, b.j1 - b.j0, b.k1 - b.k0, &st);
+  if (!gs) return st;
+  const size_t n = 6ull * (gs->nx + 1) * (gs->ny + 1) * (gs->nz + 1);
+  IE_CUDA(c, cudaMemcpyAsync(host_out, gs->oct, n * sizeof(double2), cudaMemcpyDeviceToHost, c->stream));
+  IE_CUDA(c, cudaStreamSynchronize(c->stream));
+  return IE_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,209 @@
+// Complex128 Stockham FFT building blocks for sm_100a (device code only).
+//
+// A length-L line (L = 2^p, 2 <= L <= 1024) is transformed by T = L/V threads that each
+// hold V = min(8, L) values in registers.  Each Stockham stage (Govindaraju et al. 2008
+// formulation) reads R values at stride L/R, twiddles, does a radix-R DFT in registers and
+// writes them to their auto-sorted positions; stages exchange through shared memory.
+//  * The FIRST stage takes its inputs from registers (loaded by the caller straight from
+//    global memory at positions  t + u*T + r*(L/R0)),
+//  * the LAST stage leaves its outputs in registers at positions t + u*T + r*(L/Rlast),
+// so global loads/stores are coalesced and no shared-memory staging is needed at either
+// end.  Radix order "F" is 8,8,..,(4|4,4); order "B" is its reverse -- an inverse FFT run
+// in order B starts on exactly the register positions a forward FFT in order F ends on,
+// which lets the z-pass multiply the spectrum in registers (operator.cu, K-C).
+// Twiddles come from per-stage tables tw[(r-1)*Ns + k] = exp(-2 pi i r k / (Ns R)) so
+// that lanes with consecutive k read consecutive addresses.
+#pragma once
+#include <cuda_runtime.h>
+
+namespace ie {
+
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+// a * conj(b)
+__device__ __forceinline__ double2 cmulc(double2 a, double2 b) {
+  return make_double2(fma(a.x, b.x, a.y * b.y), fma(a.y, b.x, -a.x * b.y));
+}
+__device__ __forceinline__ double2 cscale(double2 a, double s) { return make_double2(a.x * s, a.y * s); }
+__device__ __forceinline__ double2 czero() { return make_double2(0.0, 0.0); }
+
+// multiply by w4 = exp(DIR * i pi / 2) = DIR * i
+template <int DIR>
+__device__ __forceinline__ double2 mul_w4(double2 a) {
+  return DIR > 0 ? make_double2(-a.y, a.x) : make_double2(a.y, -a.x);
+}
+// multiply by w8 = exp(DIR * i pi / 4) = (1 + DIR i)/sqrt2
+template <int DIR>
+__device__ __forceinline__ double2 mul_w8(double2 a) {
+  constexpr double s = 0.70710678118654752440084436210485;
+  return DIR > 0 ? make_double2((a.x - a.y) * s, (a.y + a.x) * s) : make_double2((a.x + a.y) * s, (a.y - a.x) * s);
+}
+// multiply by w8^3 = exp(3 DIR i pi / 4) = (-1 + DIR i)/sqrt2
+template <int DIR>
+__device__ __forceinline__ double2 mul_w83(double2 a) {
+  constexpr double s = 0.70710678118654752440084436210485;
+  return DIR > 0 ? make_double2((-a.x - a.y) * s, (a.x - a.y) * s) : make_double2((a.y - a.x) * s, (-a.y - a.x) * s);
+}
+
+// In-place natural-order DFTs: X_k = sum_r v_r exp(DIR 2 pi i r k / R)
+template <int DIR>
+__device__ __forceinline__ void dft2(double2* v) {
+  double2 a = v[0], b = v[1];
+  v[0] = cadd(a, b);
+  v[1] = csub(a, b);
+}
+template <int DIR>
+__device__ __forceinline__ void dft4(double2& v0, double2& v1, double2& v2, double2& v3) {
+  double2 e0 = cadd(v0, v2), e1 = csub(v0, v2);
+  double2 o0 = cadd(v1, v3), o1 = mul_w4<DIR>(csub(v1, v3));
+  v0 = cadd(e0, o0);
+  v2 = csub(e0, o0);
+  v1 = cadd(e1, o1);
+  v3 = csub(e1, o1);
+}
+template <int DIR>
+__device__ __forceinline__ void dft4(double2* v) {
+  dft4<DIR>(v[0], v[1], v[2], v[3]);
+}
+template <int DIR>
+__device__ __forceinline__ void dft8(double2* v) {
+  double2 e0 = v[0], e1 = v[2], e2 = v[4], e3 = v[6];
+  double2 o0 = v[1], o1 = v[3], o2 = v[5], o3 = v[7];
+  dft4<DIR>(e0, e1, e2, e3);
+  dft4<DIR>(o0, o1, o2, o3);
+  o1 = mul_w8<DIR>(o1);
+  o2 = mul_w4<DIR>(o2);
+  o3 = mul_w83<DIR>(o3);
+  v[0] = cadd(e0, o0);
+  v[4] = csub(e0, o0);
+  v[1] = cadd(e1, o1);
+  v[5] = csub(e1, o1);
+  v[2] = cadd(e2, o2);
+  v[6] = csub(e2, o2);
+  v[3] = cadd(e3, o3);
+  v[7] = csub(e3, o3);
+}
+template <int R, int DIR>
+__device__ __forceinline__ void dftR(double2* v) {
+  if constexpr (R == 2) dft2<DIR>(v);
+  else if constexpr (R == 4) dft4<DIR>(v);
+  else dft8<DIR>(v);
+}
+
+// ------------------------------------------------------------------------ plans
+__host__ __device__ constexpr int log2c(int L) { return L <= 1 ? 0 : 1 + log2c(L / 2); }
+
+template <int L>
+struct FftPlan {
+  static constexpr int P = log2c(L);
+  static constexpr int NST = (P <= 3) ? 1 : (P + 2) / 3;
+  static constexpr int V = L < 8 ? L : 8;
+  static constexpr int T = L / V;
+  // forward ("F") radix order
+  __host__ __device__ static constexpr int radixF(int s) {
+    return (P <= 3) ? L : (s < ((P % 3 == 0) ? P / 3 : (P % 3 == 2) ? P / 3 : P / 3 - 1) ? 8 : 4);
+  }
+  __host__ __device__ static constexpr int radix(int s, bool rev) { return rev ? radixF(NST - 1 - s) : radixF(s); }
+  __host__ __device__ static constexpr int ns(int s, bool rev) { return s == 0 ? 1 : ns(s - 1, rev) * radix(s - 1, rev); }
+  // twiddle table offset of stage s (s >= 1): sum over earlier stages of (R-1)*Ns
+  __host__ __device__ static constexpr int twoff(int s, bool rev) {
+    return s <= 1 ? 0 : twoff(s - 1, rev) + (radix(s - 1, rev) - 1) * ns(s - 1, rev);
+  }
+  __host__ __device__ static constexpr int twsize(bool rev) { return twoff(NST, rev); }
+};
+
+// shared-memory index for element i of a column c among W interleaved columns, padded by
+// one element per 8 so that stride-8 (128-byte) lane patterns do not bank-conflict.
+struct SIdx {
+  int base, W, c;
+  __device__ __forceinline__ int operator()(int i) const {
+    int a = i * W + c;
+    return base + a + (a >> 3);
+  }
+};
+__host__ __device__ constexpr int padded(int n) { return n + (n >> 3); }
+
+// Transform NL lines held by this thread (v[l][0..V)) through all stages.
+//   entry: v[l][u*R0 + r] = x_l[t + u*T + r*L/R0]            (R0 = first radix)
+//   exit : v[l][u*RL + r] = X_l[t + u*T + r*L/RL]            (RL = last radix)
+// sm + idx(l)(i): shared-memory slot of element i of line l.  tw: twiddle table of this
+// (L, order).  need_sync_first: a __syncthreads() before the first shared write (when the
+// regions were read just before).  All threads of the CTA must call this (barriers).
+template <int L, bool REV, int DIR, int NL, int S, class IdxF>
+__device__ __forceinline__ void fft_stage(double2 (&v)[NL][FftPlan<L>::V], double2* sm, IdxF idx, int t,
+                                          const double2* __restrict__ tw) {
+  using P = FftPlan<L>;
+  constexpr int V = P::V, T = P::T, NST = P::NST;
+  constexpr int R = P::radix(S, REV);
+  constexpr int Ns = P::ns(S, REV);
+  constexpr int U = V / R;
+  const double2* tws = tw + P::twoff(S, REV);
+#pragma unroll
+  for (int l = 0; l < NL; ++l)
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int j = t + u * T;
+#pragma unroll
+      for (int r = 0; r < R; ++r) v[l][u * R + r] = sm[idx(l)(j + r * (L / R))];
+    }
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const int j = t + u * T;
+    const int k = j & (Ns - 1);
+    double2 w[R];
+#pragma unroll
+    for (int r = 1; r < R; ++r) w[r] = __ldg(&tws[(r - 1) * Ns + k]);
+#pragma unroll
+    for (int l = 0; l < NL; ++l) {
+#pragma unroll
+      for (int r = 1; r < R; ++r)
+        v[l][u * R + r] = (DIR < 0) ? cmul(v[l][u * R + r], w[r]) : cmulc(v[l][u * R + r], w[r]);
+      dftR<R, DIR>(&v[l][u * R]);
+    }
+  }
+  if constexpr (S < NST - 1) {
+    __syncthreads();
+#pragma unroll
+    for (int l = 0; l < NL; ++l)
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int j = t + u * T;
+        const int k = j & (Ns - 1);
+        const int base = (j - k) * R + k;
+#pragma unroll
+        for (int r = 0; r < R; ++r) sm[idx(l)(base + r * Ns)] = v[l][u * R + r];
+      }
+    __syncthreads();
+    fft_stage<L, REV, DIR, NL, S + 1>(v, sm, idx, t, tw);
+  }
+}
+
+template <int L, bool REV, int DIR, int NL, class IdxF>
+__device__ __forceinline__ void fft_run(double2 (&v)[NL][FftPlan<L>::V], double2* sm, IdxF idx, int t,
+                                        const double2* __restrict__ tw, bool need_sync_first) {
+  using P = FftPlan<L>;
+  constexpr int V = P::V, T = P::T, NST = P::NST;
+  constexpr int R0 = P::radix(0, REV);
+#pragma unroll
+  for (int l = 0; l < NL; ++l)
+#pragma unroll
+    for (int u = 0; u < V / R0; ++u) dftR<R0, DIR>(&v[l][u * R0]);
+  if constexpr (NST > 1) {
+    if (need_sync_first) __syncthreads();
+#pragma unroll
+    for (int l = 0; l < NL; ++l)
+#pragma unroll
+      for (int u = 0; u < V / R0; ++u) {
+        const int j = t + u * T;
+#pragma unroll
+        for (int r = 0; r < R0; ++r) sm[idx(l)(j * R0 + r)] = v[l][u * R0 + r];
+      }
+    __syncthreads();
+    fft_stage<L, REV, DIR, NL, 1>(v, sm, idx, t, tw);
+  }
+}
+
+}  // namespace ie

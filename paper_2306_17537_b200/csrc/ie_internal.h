@@ -1,0 +1,158 @@
+// Internal declarations shared by the CUDA translation units of libie_b200.so.
+// Not part of the C-ABI (that is include/ie_b200.h).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <complex>
+#include <deque>
+#include <string>
+#include <vector>
+
+#include "../../include/ie_b200.h"
+
+namespace ie {
+
+using cplx = std::complex<double>;
+constexpr double kPi = 3.14159265358979323846264338327950288;
+constexpr double kMu0 = 4e-7 * kPi;  // DESIGN.md reading R1
+constexpr int kMaxItems = 48;        // batch items per operator launch (kernel-parameter budget)
+constexpr int kMaxLog2 = 10;         // FFT lengths 2 .. 1024
+
+// -------------------------------------------------------------------- operator batch
+// One operator application on one right-hand side / sub-domain.  The operator's domain is
+// an (nx,ny,nz) box; the source (contrast) region is the sub-box [s?0, s?1) of it and the
+// input x is compact over that sub-box.  y = alpha*xs*x + beta*conv + (accumulate ? y : 0),
+// conv = G (dsigma * xs * x) on the domain, xs = xscale.
+struct ApplyItem {
+  const double2* x;    // [3][sz][sy][sx] over the source sub-box
+  double2* y;          // [3][nz][ny][nx] over the domain
+  const double* dsig;  // sym6 dsigma at domain cell (0,0,0); strides in ApplyParams
+  double xscale;
+  int sx0, sx1, sy0, sy1, sz0, sz1;
+};
+
+struct ApplyParams {
+  int nx, ny, nz;
+  long long ds_cs, ds_zs, ds_ys;  // dsigma strides (doubles): component, z, y (x stride 1)
+  const double2* ghat;            // packed spectrum [6][nz+1][ny+1][nx+1]
+  double2* X1;                    // [item][3][nz][ny][2nx]
+  double2* X2;                    // [item][3][nz][2ny][2nx]
+  double alpha, beta;
+  int accumulate;
+  const double2* tw_x;   // twiddles, L = 2nx, forward radix order
+  const double2* tw_y;   // L = 2ny, forward order
+  const double2* tw_z;   // L = 2nz, forward order
+  const double2* tw_zr;  // L = 2nz, reversed order
+  int n_items;
+  ApplyItem items[kMaxItems];
+};
+
+struct Twiddles {
+  double2* dev = nullptr;
+  int off[kMaxLog2 + 1][2] = {};  // [log2 L][order]
+  const double2* get(int L, int rev) const;
+};
+
+struct GreenSpec {
+  int nx, ny, nz;
+  double2* oct = nullptr;  // [6][nz+1][ny+1][nx+1]
+};
+
+// workspace bump allocator (caller-owned memory)
+struct Arena {
+  char* base = nullptr;
+  size_t cap = 0, used = 0, peak = 0;
+  bool counting = false;  // size-query mode: no memory, only accounting
+  void* take(size_t bytes);
+};
+
+}  // namespace ie
+
+struct ie_ctx {
+  ie_grid g;
+  double sigma_b = 0, freq = 0, omega = 0;
+  ie::cplx k0, self;
+  cudaStream_t stream = nullptr;
+  ie::Twiddles tw;
+  std::deque<ie::GreenSpec> greens;  // [0] = whole grid (deque: stable element addresses)
+  double* dsig = nullptr;             // sym6 [6][nz][ny][nx]
+  double2* e0 = nullptr;
+  int n_src = 0;
+  std::vector<double> src_pos, src_mom;  // host copies of the dipoles (for H0 at receivers)
+  bool contrast_set = false;
+  char* ws = nullptr;
+  size_t ws_bytes = 0;
+  std::string err;
+  long long launches = 0;
+  // small pinned host staging for reductions / coefficients
+  double2* h_red = nullptr;
+  size_t h_red_cap = 0;
+  double2* d_red = nullptr;  // device mirror for coefficient uploads
+  size_t d_red_cap = 0;
+};
+
+namespace ie {
+
+// ------------------------------------------------------------------ status helpers
+ie_status fail(ie_ctx* c, ie_status s, const std::string& msg);
+ie_status cuda_fail(ie_ctx* c, cudaError_t e, const char* where);
+#define IE_CUDA(ctx, call)                                           \
+  do {                                                               \
+    cudaError_t e__ = (call);                                        \
+    if (e__ != cudaSuccess) return ie::cuda_fail((ctx), e__, #call); \
+  } while (0)
+#define IE_CHECK_LAUNCH(ctx, name)                                     \
+  do {                                                                 \
+    (ctx)->launches++;                                                 \
+    cudaError_t e__ = cudaGetLastError();                              \
+    if (e__ != cudaSuccess) return ie::cuda_fail((ctx), e__, (name)); \
+  } while (0)
+
+inline bool is_pow2(long long v) { return v >= 1 && (v & (v - 1)) == 0; }
+inline int ilog2i(long long v) {
+  int p = 0;
+  while ((1LL << p) < v) ++p;
+  return p;
+}
+
+// ----------------------------------------------------------------- entry points (internal)
+// operator.cu
+ie_status build_twiddles(ie_ctx* c);
+ie_status launch_apply(ie_ctx* c, ApplyParams& p);  // p.items/n_items may exceed kMaxItems? no: caller splits
+size_t apply_scratch_bytes(int nx, int ny, int nz, int n_items);
+// green.cu
+ie_status build_green(ie_ctx* c, int nx, int ny, int nz, GreenSpec* out);
+const GreenSpec* green_for(ie_ctx* c, int nx, int ny, int nz, ie_status* st);
+// fields.cu
+ie_status pack_contrast(ie_ctx* c, const void* sigma_dev, int layout);
+ie_status compute_incident(ie_ctx* c, int n_src, const double* pos, const double* moment, double2* out);
+ie_status receivers(ie_ctx* c, const double2* e, int n_rx, const double* rx, cplx* h_out, const double* src_pos,
+                    const double* src_mom, int n_src, double2* scratch /* >= (296 + n_src*n_rx)*3 */);
+void launch_gather(ie_ctx* c, const double2* full, double2* box, const ie_box& b, int nsys, long long full_stride,
+                   long long box_stride);
+void launch_scatter(ie_ctx* c, double2* full, const double2* box, const ie_box& b, int nsys, long long full_stride,
+                    long long box_stride);
+void launch_axpby(ie_ctx* c, double2* z, cplx a, const double2* x, cplx b, const double2* y, long long n);
+// sums of |a - b|^2 (b may be null) per system; result doubles on host
+ie_status norms2(ie_ctx* c, const double2* a, const double2* b, int nsys, long long len, long long stride,
+                 double* out_host);
+// krylov.cu
+struct GmresSystem {
+  const double2* b;  // rhs (compact over the domain)
+  double2* x;        // initial guess in, solution out
+  const double* dsig;
+  double tol;
+  int min_iters;
+};
+struct GmresResult {
+  int iters = 0, restarts = 0, converged = 0, breakdown = 0;
+  double relres_est = 0, relres_true = 0;
+};
+ie_status gmres_batched(ie_ctx* c, Arena& ar, int nx, int ny, int nz, long long ds_zs, long long ds_ys,
+                        const std::vector<GmresSystem>& sys, int restart, int max_iters,
+                        std::vector<GmresResult>& res, long long* applies);
+size_t gmres_scratch_bytes(int nx, int ny, int nz, int nsys, int restart);
+
+}  // namespace ie

@@ -1,0 +1,487 @@
+// Restarted GMRES (Saad & Schultz 1986) batched over independent systems that
+// share one operator shape (the right-hand sides of one domain, or the equal-shape
+// sub-domains of a Jacobi sweep).  Device side: the operator (operator.cu), fused
+// multi-vector dot products (w read once per 16 basis vectors), fused multi-axpy, fixed-order
+// reductions.  Host side: Hessenberg / Givens recurrences (O(m^2) scalars per system).
+//
+// Orthogonalisation: classical Gram-Schmidt with the DGKS re-orthogonalisation test
+// (repeat once if ||w_after||^2 < 0.5 ||w_before||^2, using ||w_after||^2 = ||w||^2 -
+// sum |h_j|^2); the basis is kept unnormalised with a per-vector scale 1/beta that the next
+// operator application folds into its load (ApplyItem::xscale).
+#include <math.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "fft_core.cuh"
+#include "ie_internal.h"
+
+namespace ie {
+
+constexpr int kDotG = 16;  // basis vectors per pass over w
+
+struct DotJob {
+  const double2* w;
+  const double2* V;  // first basis vector; vector j at V + j * len
+  int nv;            // number of basis vectors (dots); row nv gets ||w||^2 in .x
+  int row;           // output row base
+};
+struct AxpyJob {
+  double2* out;
+  const double2* base;  // may be null (then 0)
+  const double2* V;
+  int nv;
+  int coef;  // offset into the coefficient array
+};
+
+__device__ __forceinline__ double2 shfl_down2(double2 v, int d) {
+  return make_double2(__shfl_down_sync(0xffffffffu, v.x, d), __shfl_down_sync(0xffffffffu, v.y, d));
+}
+
+__global__ void __launch_bounds__(256) k_mdot(const DotJob* __restrict__ jobs, long long len, double2* __restrict__ part,
+                                              int nblk) {
+  const DotJob jb = jobs[blockIdx.y];
+  __shared__ double2 red[8][kDotG];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int j0 = 0; j0 <= jb.nv; j0 += kDotG) {
+    double2 acc[kDotG];
+#pragma unroll
+    for (int g = 0; g < kDotG; ++g) acc[g] = czero();
+    for (long long i = blockIdx.x * 256LL + threadIdx.x; i < len; i += (long long)nblk * 256) {
+      const double2 w = jb.w[i];
+#pragma unroll
+      for (int g = 0; g < kDotG; ++g) {
+        const int j = j0 + g;
+        if (j < jb.nv) {
+          const double2 v = jb.V[(long long)j * len + i];
+          acc[g].x = fma(v.x, w.x, fma(v.y, w.y, acc[g].x));  // conj(v) * w
+          acc[g].y = fma(v.x, w.y, fma(-v.y, w.x, acc[g].y));
+        } else if (j == jb.nv) {
+          acc[g].x = fma(w.x, w.x, fma(w.y, w.y, acc[g].x));
+        }
+      }
+    }
+#pragma unroll
+    for (int g = 0; g < kDotG; ++g) {
+#pragma unroll
+      for (int d = 16; d > 0; d >>= 1) acc[g] = cadd(acc[g], shfl_down2(acc[g], d));
+    }
+    if (lane == 0)
+#pragma unroll
+      for (int g = 0; g < kDotG; ++g) red[wid][g] = acc[g];
+    __syncthreads();
+    if (threadIdx.x < kDotG) {
+      const int j = j0 + threadIdx.x;
+      double2 s = czero();
+      for (int w8 = 0; w8 < 8; ++w8) s = cadd(s, red[w8][threadIdx.x]);
+      if (j <= jb.nv) part[(long long)(jb.row + j) * nblk + blockIdx.x] = s;
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void k_reduce_rows(const double2* __restrict__ part, int nblk, double2* __restrict__ out) {
+  const int row = blockIdx.x;
+  __shared__ double2 red[128];
+  double2 s = czero();
+  for (int i = threadIdx.x; i < nblk; i += blockDim.x) s = cadd(s, part[(long long)row * nblk + i]);
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int k = blockDim.x / 2; k > 0; k >>= 1) {
+    if ((int)threadIdx.x < k) red[threadIdx.x] = cadd(red[threadIdx.x], red[threadIdx.x + k]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[row] = red[0];
+}
+
+__global__ void __launch_bounds__(256) k_maxpy(const AxpyJob* __restrict__ jobs, const double2* __restrict__ coefs,
+                                               long long len) {
+  const AxpyJob jb = jobs[blockIdx.y];
+  __shared__ double2 cf[160];
+  for (int j = threadIdx.x; j < jb.nv; j += blockDim.x) cf[j] = coefs[jb.coef + j];
+  __syncthreads();
+  for (long long i = blockIdx.x * 256LL + threadIdx.x; i < len; i += (long long)gridDim.x * 256) {
+    double2 a0 = jb.base ? jb.base[i] : czero(), a1 = czero();
+    int j = 0;
+    for (; j + 1 < jb.nv; j += 2) {
+      const double2 v0 = jb.V[(long long)j * len + i], v1 = jb.V[(long long)(j + 1) * len + i];
+      a0 = cadd(a0, cmul(cf[j], v0));
+      a1 = cadd(a1, cmul(cf[j + 1], v1));
+    }
+    if (j < jb.nv) a0 = cadd(a0, cmul(cf[j], jb.V[(long long)j * len + i]));
+    jb.out[i] = cadd(a0, a1);
+  }
+}
+
+// ------------------------------------------------------------------------ host
+void* Arena::take(size_t bytes) {
+  const size_t a = (used + 255) & ~(size_t)255;
+  used = a + bytes;
+  if (used > peak) peak = used;
+  if (counting || used > cap) return nullptr;
+  return base + a;
+}
+
+size_t gmres_scratch_bytes(int nx, int ny, int nz, int nsys, int restart) {
+  const size_t len = 3ull * nx * ny * nz;
+  const int items = std::min(nsys, kMaxItems);
+  const int nblk = 64;
+  size_t b = 0;
+  auto add = [&](size_t x) { b = ((b + 255) & ~(size_t)255) + x; };
+  add((size_t)nsys * (restart + 1) * len * sizeof(double2));           // V
+  add(apply_scratch_bytes(nx, ny, nz, items));                          // X1/X2
+  add((size_t)nsys * (restart + 2) * nblk * sizeof(double2));           // partials
+  add((size_t)nsys * (restart + 2) * sizeof(double2));                  // reduced rows
+  add((size_t)nsys * (restart + 2) * sizeof(double2) + nsys * 64 * 2);  // jobs + coefficients
+  add(4096);
+  return b + 1024;
+}
+
+namespace {
+
+struct SysState {
+  std::vector<cplx> H;  // (m+1) x m, column-major: H[k*(m+1) + j]
+  std::vector<cplx> cs, sn, g;
+  std::vector<double> scale;
+  double bnorm = 0, beta = 0;
+  int k = 0;          // Arnoldi steps in the current cycle
+  bool active = true;  // still being solved
+  bool cycle = false;  // iterating in the current cycle
+};
+
+}  // namespace
+
+ie_status gmres_batched(ie_ctx* c, Arena& ar, int nx, int ny, int nz, long long ds_zs, long long ds_ys,
+                        const std::vector<GmresSystem>& sys, int m, int max_iters, std::vector<GmresResult>& res,
+                        long long* applies) {
+  const int S = (int)sys.size();
+  res.assign(S, GmresResult());
+  if (S == 0) return IE_OK;
+  const long long N = (long long)nx * ny * nz, len = 3 * N;
+  const int items = std::min(S, kMaxItems);
+  const int nblk = 64;
+  ie_status st;
+  const GreenSpec* gs = green_for(c, nx, ny, nz, &st);
+  if (!gs) return st;
+  // staging (host pinned + device mirror): [dot jobs S*64 | axpy jobs S*64 | coefs S*(m+2)*16]
+  const size_t jobs_bytes = (size_t)S * 64 * 2 + (size_t)S * (m + 2) * sizeof(double2);
+  double2* V = (double2*)ar.take((size_t)S * (m + 1) * len * sizeof(double2));
+  double2* scratch = (double2*)ar.take(apply_scratch_bytes(nx, ny, nz, items));
+  double2* part = (double2*)ar.take((size_t)S * (m + 2) * nblk * sizeof(double2));
+  double2* rows = (double2*)ar.take((size_t)S * (m + 2) * sizeof(double2));
+  char* dstage = (char*)ar.take(jobs_bytes);
+  if (!V || !scratch || !part || !rows || !dstage)
+    return fail(c, IE_ERR_OUT_OF_MEMORY, "workspace too small for GMRES (need " + std::to_string(ar.peak) +
+                                             " bytes; see ie_workspace_query)");
+  const size_t rows_bytes = (size_t)S * (m + 2) * sizeof(double2);
+  const size_t hneed = rows_bytes + jobs_bytes + 256;
+  if (c->h_red_cap < hneed) {
+    if (c->h_red) cudaFreeHost(c->h_red);
+    c->h_red = nullptr;
+    IE_CUDA(c, cudaMallocHost(&c->h_red, hneed));
+    c->h_red_cap = hneed;
+  }
+  char* hstage = (char*)c->h_red;
+  double2* hrows = (double2*)hstage;  // results of reductions
+  DotJob* h_dot = (DotJob*)(hstage + rows_bytes);
+  AxpyJob* h_axpy = (AxpyJob*)(hstage + rows_bytes + (size_t)S * 64);
+  double2* h_coef = (double2*)(hstage + rows_bytes + (size_t)S * 128);
+  DotJob* d_dot = (DotJob*)dstage;
+  AxpyJob* d_axpy = (AxpyJob*)(dstage + (size_t)S * 64);
+  double2* d_coef = (double2*)(dstage + (size_t)S * 128);
+
+  auto Vs = [&](int s, int j) { return V + ((long long)s * (m + 1) + j) * len; };
+
+  ApplyParams ap;
+  ap.nx = nx;
+  ap.ny = ny;
+  ap.nz = nz;
+  ap.ds_cs = (long long)c->g.nx * c->g.ny * c->g.nz;
+  ap.ds_zs = ds_zs;
+  ap.ds_ys = ds_ys;
+  ap.ghat = gs->oct;
+  ap.X1 = scratch;
+  ap.X2 = scratch + (size_t)items * 3 * 2 * N;
+  // apply to a list of (system, input, output) with given coefficients
+  auto apply = [&](const std::vector<int>& ids, std::vector<const double2*> xin, std::vector<double> xsc,
+                   std::vector<double2*> yout, double alpha, double beta, int acc) -> ie_status {
+    for (size_t b0 = 0; b0 < ids.size(); b0 += kMaxItems) {
+      const int nb = (int)std::min<size_t>(kMaxItems, ids.size() - b0);
+      ap.alpha = alpha;
+      ap.beta = beta;
+      ap.accumulate = acc;
+      ap.n_items = nb;
+      for (int i = 0; i < nb; ++i) {
+        ApplyItem& it = ap.items[i];
+        it.x = xin[b0 + i];
+        it.y = yout[b0 + i];
+        it.dsig = sys[ids[b0 + i]].dsig;
+        it.xscale = xsc[b0 + i];
+        it.sx0 = 0;
+        it.sx1 = nx;
+        it.sy0 = 0;
+        it.sy1 = ny;
+        it.sz0 = 0;
+        it.sz1 = nz;
+      }
+      ie_status s2 = launch_apply(c, ap);
+      if (s2) return s2;
+      if (applies) *applies += nb;
+    }
+    return IE_OK;
+  };
+  // dots: for each id, rows [row_base + 0 .. nv] = <V_j, w> (j < nv), ||w||^2 ; returns on host
+  auto dots = [&](const std::vector<int>& ids, const std::vector<const double2*>& w, const std::vector<int>& nv,
+                  std::vector<int>& rowbase) -> ie_status {
+    const int n = (int)ids.size();
+    DotJob* hj = h_dot;
+    int row = 0;
+    rowbase.resize(n);
+    for (int i = 0; i < n; ++i) {
+      hj[i] = DotJob{w[i], Vs(ids[i], 0), nv[i], row};
+      rowbase[i] = row;
+      row += nv[i] + 1;
+    }
+    IE_CUDA(c, cudaMemcpyAsync(d_dot, hj, n * sizeof(DotJob), cudaMemcpyHostToDevice, c->stream));
+    k_mdot<<<dim3(nblk, n), 256, 0, c->stream>>>(d_dot, len, part, nblk);
+    IE_CHECK_LAUNCH(c, "k_mdot");
+    k_reduce_rows<<<row, 128, 0, c->stream>>>(part, nblk, rows);
+    IE_CHECK_LAUNCH(c, "k_reduce_rows");
+    IE_CUDA(c, cudaMemcpyAsync(hrows, rows, row * sizeof(double2), cudaMemcpyDeviceToHost, c->stream));
+    IE_CUDA(c, cudaStreamSynchronize(c->stream));
+    return IE_OK;
+  };
+  // axpy: out_i = base_i + sum_j coef_ij V_ij
+  auto axpy = [&](const std::vector<AxpyJob>& jobs, const std::vector<cplx>& coefs) -> ie_status {
+    const int n = (int)jobs.size();
+    if (n == 0) return IE_OK;
+    for (int i = 0; i < n; ++i) h_axpy[i] = jobs[i];
+    for (size_t i = 0; i < coefs.size(); ++i) h_coef[i] = make_double2(coefs[i].real(), coefs[i].imag());
+    IE_CUDA(c, cudaMemcpyAsync(d_axpy, h_axpy, n * sizeof(AxpyJob), cudaMemcpyHostToDevice, c->stream));
+    IE_CUDA(c, cudaMemcpyAsync(d_coef, h_coef, coefs.size() * sizeof(double2), cudaMemcpyHostToDevice, c->stream));
+    const int gx = (int)std::max<long long>(1, std::min<long long>((len + 255) / 256, 1184 / n + 1));
+    k_maxpy<<<dim3(gx, n), 256, 0, c->stream>>>(d_axpy, d_coef, len);
+    IE_CHECK_LAUNCH(c, "k_maxpy");
+    return IE_OK;
+  };
+
+  std::vector<SysState> ss(S);
+  for (auto& s : ss) {
+    s.H.assign((size_t)(m + 1) * m, 0.0);
+    s.cs.assign(m, 0.0);
+    s.sn.assign(m, 0.0);
+    s.g.assign(m + 1, 0.0);
+    s.scale.assign(m + 1, 1.0);
+  }
+  // ||b||
+  {
+    std::vector<double> nb(S);
+    for (int s = 0; s < S; ++s) {
+      double v;
+      st = norms2(c, sys[s].b, nullptr, 1, len, 0, &v);
+      if (st) return st;
+      nb[s] = sqrt(v);
+      ss[s].bnorm = nb[s];
+    }
+  }
+  // true residual r = b - A x into V[s][0]; beta, relres_true
+  auto residual = [&](const std::vector<int>& ids) -> ie_status {
+    std::vector<const double2*> xin;
+    std::vector<double> xsc;
+    std::vector<double2*> yo;
+    for (int s : ids) {
+      launch_axpby(c, Vs(s, 0), 1.0, sys[s].b, 0.0, nullptr, len);
+      xin.push_back(sys[s].x);
+      xsc.push_back(1.0);
+      yo.push_back(Vs(s, 0));
+    }
+    ie_status s2 = apply(ids, xin, xsc, yo, -1.0, 1.0, 1);  // V0 = b - x + G dsigma x
+    if (s2) return s2;
+    for (int s : ids) {
+      double v;
+      s2 = norms2(c, Vs(s, 0), nullptr, 1, len, 0, &v);
+      if (s2) return s2;
+      ss[s].beta = sqrt(v);
+      res[s].relres_true = ss[s].bnorm > 0 ? ss[s].beta / ss[s].bnorm : 0.0;
+      if (!std::isfinite(v)) res[s].breakdown = 1;
+    }
+    return IE_OK;
+  };
+  std::vector<int> all;
+  for (int s = 0; s < S; ++s) {
+    if (ss[s].bnorm == 0.0) {  // b = 0 -> x = 0
+      launch_axpby(c, sys[s].x, 0.0, sys[s].x, 0.0, nullptr, len);
+      ss[s].active = false;
+      res[s].converged = 1;
+      continue;
+    }
+    all.push_back(s);
+  }
+  st = residual(all);
+  if (st) return st;
+  for (int s : all) {
+    res[s].relres_est = res[s].relres_true;
+    if (res[s].breakdown) ss[s].active = false;
+    else if (res[s].relres_true <= sys[s].tol && sys[s].min_iters <= 0) {
+      ss[s].active = false;
+      res[s].converged = 1;
+    } else if (max_iters <= 0) {
+      ss[s].active = false;
+    }
+  }
+
+  while (true) {
+    std::vector<int> act;
+    for (int s = 0; s < S; ++s)
+      if (ss[s].active) act.push_back(s);
+    if (act.empty()) break;
+    for (int s : act) {
+      SysState& q = ss[s];
+      q.scale[0] = 1.0 / q.beta;
+      std::fill(q.g.begin(), q.g.end(), cplx(0.0));
+      q.g[0] = q.beta;
+      q.k = 0;
+      q.cycle = true;
+    }
+    for (int k = 0; k < m; ++k) {
+      std::vector<int> it;
+      for (int s : act)
+        if (ss[s].cycle) it.push_back(s);
+      if (it.empty()) break;
+      // w = A v_k  -> V[s][k+1]
+      std::vector<const double2*> xin;
+      std::vector<double> xsc;
+      std::vector<double2*> yo;
+      for (int s : it) {
+        xin.push_back(Vs(s, k));
+        xsc.push_back(ss[s].scale[k]);
+        yo.push_back(Vs(s, k + 1));
+      }
+      st = apply(it, xin, xsc, yo, 1.0, -1.0, 0);
+      if (st) return st;
+      std::vector<std::vector<cplx>> h(it.size(), std::vector<cplx>(k + 1, 0.0));
+      std::vector<double> beta2(it.size());
+      std::vector<int> todo(it.size());
+      for (size_t i = 0; i < it.size(); ++i) todo[i] = (int)i;
+      for (int pass = 0; pass < 2 && !todo.empty(); ++pass) {
+        std::vector<int> ids;
+        std::vector<const double2*> w;
+        std::vector<int> nv, rb;
+        for (int i : todo) {
+          ids.push_back(it[i]);
+          w.push_back(Vs(it[i], k + 1));
+          nv.push_back(k + 1);
+        }
+        st = dots(ids, w, nv, rb);
+        if (st) return st;
+        std::vector<AxpyJob> jobs;
+        std::vector<cplx> coefs;
+        std::vector<int> again;
+        for (size_t t = 0; t < todo.size(); ++t) {
+          const int i = todo[t], s = it[i];
+          const double2* r = hrows + rb[t];
+          const double ww = r[k + 1].x;
+          double hs = 0;
+          jobs.push_back(AxpyJob{Vs(s, k + 1), Vs(s, k + 1), Vs(s, 0), k + 1, (int)coefs.size()});
+          for (int j = 0; j <= k; ++j) {
+            const cplx hj = cplx(r[j].x, r[j].y) * ss[s].scale[j];
+            h[i][j] += hj;
+            hs += std::norm(hj);
+            coefs.push_back(-hj * ss[s].scale[j]);
+          }
+          beta2[i] = ww - hs;
+          if (!std::isfinite(ww) || !std::isfinite(hs)) res[s].breakdown = 1;
+          else if (pass == 0 && beta2[i] < 0.5 * ww) again.push_back(i);  // DGKS: re-orthogonalise
+        }
+        st = axpy(jobs, coefs);
+        if (st) return st;
+        todo = again;
+      }
+      for (size_t i = 0; i < it.size(); ++i) {
+        const int s = it[i];
+        SysState& q = ss[s];
+        GmresResult& rr = res[s];
+        rr.iters++;
+        if (rr.breakdown) {
+          q.cycle = false;
+          q.active = false;
+          continue;
+        }
+        const double beta = sqrt(std::max(beta2[i], 0.0));
+        cplx* Hk = &q.H[(size_t)k * (m + 1)];
+        for (int j = 0; j <= k; ++j) Hk[j] = h[i][j];
+        Hk[k + 1] = beta;
+        for (int j = 0; j < k; ++j) {  // previous rotations
+          const cplx t = q.cs[j] * Hk[j] + q.sn[j] * Hk[j + 1];
+          Hk[j + 1] = -std::conj(q.sn[j]) * Hk[j] + std::conj(q.cs[j]) * Hk[j + 1];
+          Hk[j] = t;
+        }
+        const cplx a = Hk[k], bb = Hk[k + 1];
+        const double den = sqrt(std::norm(a) + std::norm(bb));
+        if (den == 0.0) {
+          q.cs[k] = 1.0;
+          q.sn[k] = 0.0;
+        } else {
+          q.cs[k] = std::conj(a / den);
+          q.sn[k] = std::conj(bb / den);
+        }
+        Hk[k] = q.cs[k] * a + q.sn[k] * bb;
+        Hk[k + 1] = 0.0;
+        q.g[k + 1] = -std::conj(q.sn[k]) * q.g[k];
+        q.g[k] = q.cs[k] * q.g[k];
+        q.k = k + 1;
+        rr.relres_est = std::abs(q.g[k + 1]) / q.bnorm;
+        const bool happy = !(beta > 1e-14 * std::abs(Hk[k]));
+        if ((rr.relres_est <= sys[s].tol && rr.iters >= sys[s].min_iters) || rr.iters >= max_iters || happy)
+          q.cycle = false;
+        else
+          q.scale[k + 1] = 1.0 / beta;
+      }
+    }
+    // end of cycle: x += V y  (upper-triangular solve on host), then the true residual
+    std::vector<AxpyJob> jobs;
+    std::vector<cplx> coefs;
+    std::vector<int> upd;
+    for (int s : act) {
+      SysState& q = ss[s];
+      if (q.k == 0) continue;
+      const int kk = q.k;
+      std::vector<cplx> y(kk);
+      for (int j = kk - 1; j >= 0; --j) {
+        cplx t = q.g[j];
+        for (int l = j + 1; l < kk; ++l) t -= q.H[(size_t)l * (m + 1) + j] * y[l];
+        y[j] = t / q.H[(size_t)j * (m + 1) + j];
+      }
+      jobs.push_back(AxpyJob{sys[s].x, sys[s].x, Vs(s, 0), kk, (int)coefs.size()});
+      for (int j = 0; j < kk; ++j) coefs.push_back(y[j] * q.scale[j]);
+      upd.push_back(s);
+    }
+    st = axpy(jobs, coefs);
+    if (st) return st;
+    std::vector<int> live;
+    for (int s : act)
+      if (!res[s].breakdown) live.push_back(s);
+    st = residual(live);
+    if (st) return st;
+    for (int s : act) {
+      SysState& q = ss[s];
+      GmresResult& rr = res[s];
+      if (rr.breakdown) {
+        q.active = false;
+        continue;
+      }
+      if (rr.relres_true <= sys[s].tol && rr.iters >= sys[s].min_iters) {
+        rr.converged = 1;
+        q.active = false;
+      } else if (rr.iters >= max_iters || q.beta == 0.0) {
+        q.active = false;
+        rr.converged = q.beta == 0.0;
+      } else {
+        rr.restarts++;
+      }
+    }
+  }
+  return IE_OK;
+}
+
+}  // namespace ie

@@ -1,0 +1,452 @@
+// The FFT-accelerated IE operator  y = alpha x + beta G(dsigma x)   (Eq. 8 / Eq. 10,
+// P:60-74) as five sm_100a kernels over a 2x zero-padded grid:
+//   K-A k_xfwd : J = dsigma * x fused into the load, zero-pad x, length-2nx forward FFT
+//   K-B k_yfwd : zero-pad y, length-2ny forward FFT (tiles of W consecutive kx)
+//   K-C k_zconv: per (kx,ky) column: forward z FFT (upper half zero) -> 3x3 spectral
+//                multiply with the packed Green spectrum (in registers) -> inverse z FFT
+//                -> crop; written in place
+//   K-D k_yinv : inverse y FFT, keep the first ny rows
+//   K-E k_xinv : inverse x FFT, keep the first nx, y = alpha*x + beta*conv (+ y)
+// The 1/(8 nx ny nz) normalisation is folded into the packed spectrum (green.cu).
+// See DESIGN.md §Kernels for the traffic model (1344 N + 96 (nx+1)(ny+1)(nz+1) bytes).
+#include <math.h>
+
+#include <unordered_map>
+#include <vector>
+
+#include "fft_core.cuh"
+#include "ie_internal.h"
+
+namespace ie {
+
+__device__ __forceinline__ double2 ld2(const double2* p) { return __ldg(p); }
+
+// =====================================================================  K-A
+template <int L>
+__global__ void __launch_bounds__(256) k_xfwd(const __grid_constant__ ApplyParams p) {
+  using P = FftPlan<L>;
+  constexpr int T = P::T, V = P::V, R0 = P::radix(0, false), RL = P::radix(P::NST - 1, false);
+  extern __shared__ double2 sm[];
+  const ApplyItem& it = p.items[blockIdx.y];
+  const int rows_cta = blockDim.x / T;
+  const int lr = threadIdx.x / T, t = threadIdx.x % T;
+  const int sbx = it.sx1 - it.sx0, sby = it.sy1 - it.sy0, sbz = it.sz1 - it.sz0;
+  const int row = blockIdx.x * rows_cta + lr;
+  const bool valid = row < sby * sbz;
+  const int yy = valid ? it.sy0 + row % sby : 0;
+  const int zz = valid ? it.sz0 + row / sby : 0;
+  const long long sN = (long long)sbx * sby * sbz;
+  const double2* xrow = it.x + ((long long)(zz - it.sz0) * sby + (yy - it.sy0)) * sbx - it.sx0;
+  const double* srow = it.dsig + zz * p.ds_zs + yy * p.ds_ys;
+  const double xs = it.xscale;
+
+  double2 v[3][V];
+#pragma unroll
+  for (int u = 0; u < V / R0; ++u)
+#pragma unroll
+    for (int r = 0; r < R0; ++r) {
+      const int x = t + u * T + r * (L / R0);
+      double2 J0 = czero(), J1 = czero(), J2 = czero();
+      if (r < R0 / 2 && valid && x >= it.sx0 && x < it.sx1) {  // r >= R0/2 <=> x >= nx: zero padding
+        const double2 e0 = cscale(ld2(xrow + x), xs);
+        const double2 e1 = cscale(ld2(xrow + sN + x), xs);
+        const double2 e2 = cscale(ld2(xrow + 2 * sN + x), xs);
+        const double sxx = __ldg(srow + x), syy = __ldg(srow + p.ds_cs + x), szz = __ldg(srow + 2 * p.ds_cs + x);
+        const double sxy = __ldg(srow + 3 * p.ds_cs + x), sxz = __ldg(srow + 4 * p.ds_cs + x),
+                     syz = __ldg(srow + 5 * p.ds_cs + x);
+        J0 = make_double2(sxx * e0.x + sxy * e1.x + sxz * e2.x, sxx * e0.y + sxy * e1.y + sxz * e2.y);
+        J1 = make_double2(sxy * e0.x + syy * e1.x + syz * e2.x, sxy * e0.y + syy * e1.y + syz * e2.y);
+        J2 = make_double2(sxz * e0.x + syz * e1.x + szz * e2.x, sxz * e0.y + syz * e1.y + szz * e2.y);
+      }
+      v[0][u * R0 + r] = J0;
+      v[1][u * R0 + r] = J1;
+      v[2][u * R0 + r] = J2;
+    }
+  const int region = padded(L);
+  auto idx = [&](int l) { return SIdx{(lr * 3 + l) * region, 1, 0}; };
+  fft_run<L, false, -1, 3>(v, sm, idx, t, p.tw_x, false);
+  if (!valid) return;
+#pragma unroll
+  for (int l = 0; l < 3; ++l) {
+    double2* out = p.X1 + ((((long long)blockIdx.y * 3 + l) * p.nz + zz) * p.ny + yy) * L;
+#pragma unroll
+    for (int u = 0; u < V / RL; ++u)
+#pragma unroll
+      for (int r = 0; r < RL; ++r) out[t + u * T + r * (L / RL)] = v[l][u * RL + r];
+  }
+}
+
+// =====================================================================  K-B
+template <int L>
+__global__ void __launch_bounds__(512) k_yfwd(const __grid_constant__ ApplyParams p) {
+  using P = FftPlan<L>;
+  constexpr int T = P::T, V = P::V, R0 = P::radix(0, false), RL = P::radix(P::NST - 1, false);
+  extern __shared__ double2 sm[];
+  const int W = blockDim.x / T;
+  const int c = threadIdx.x % W, t = threadIdx.x / W;
+  const int item = blockIdx.z / 3, q = blockIdx.z % 3;
+  const ApplyItem& it = p.items[item];
+  const int Lx = 2 * p.nx;
+  const int kx = blockIdx.x * W + c;
+  const int z = it.sz0 + blockIdx.y;
+  const double2* src = p.X1 + (((long long)item * 3 + q) * p.nz + z) * p.ny * Lx + kx;
+  double2 v[1][V];
+#pragma unroll
+  for (int u = 0; u < V / R0; ++u)
+#pragma unroll
+    for (int r = 0; r < R0; ++r) {
+      const int y = t + u * T + r * (L / R0);
+      v[0][u * R0 + r] = (r < R0 / 2 && y >= it.sy0 && y < it.sy1) ? src[(long long)y * Lx] : czero();
+    }
+  auto idx = [&](int) { return SIdx{0, W, c}; };
+  fft_run<L, false, -1, 1>(v, sm, idx, t, p.tw_y, false);
+  double2* dst = p.X2 + (((long long)item * 3 + q) * p.nz + z) * (long long)L * Lx + kx;
+#pragma unroll
+  for (int u = 0; u < V / RL; ++u)
+#pragma unroll
+    for (int r = 0; r < RL; ++r) dst[(long long)(t + u * T + r * (L / RL)) * Lx] = v[0][u * RL + r];
+}
+
+// =====================================================================  K-C
+template <int L>
+__global__ void __launch_bounds__(256) k_zconv(const __grid_constant__ ApplyParams p) {
+  using P = FftPlan<L>;
+  constexpr int T = P::T, V = P::V;
+  constexpr int R0 = P::radix(0, false), RF = P::radix(P::NST - 1, false);  // forward order F
+  constexpr int RB0 = P::radix(0, true), RBL = P::radix(P::NST - 1, true);  // inverse in order B
+  static_assert(RB0 == RF && RBL == R0, "order B reverses order F");
+  extern __shared__ double2 sm[];
+  const int W = blockDim.x / T;
+  const int c = threadIdx.x % W, t = threadIdx.x / W;
+  const int item = blockIdx.z;
+  const ApplyItem& it = p.items[item];
+  const int nx = p.nx, ny = p.ny, nz = p.nz, Lx = 2 * nx, Ly = 2 * ny;
+  const int kx = blockIdx.x * W + c;
+  // mirror pairs (ky, 2ny-ky) adjacent in launch order so their shared octant rows hit L2
+  const int by = blockIdx.y;
+  const int ky = (by == 0) ? 0 : (by == 1 ? ny : ((by & 1) ? Ly - (by >> 1) : (by >> 1)));
+  const long long cs = (long long)nz * Ly * Lx;  // component stride
+  double2* col = p.X2 + (long long)item * 3 * cs + (long long)ky * Lx + kx;
+  const long long zs = (long long)Ly * Lx;
+
+  double2 v[3][V];
+#pragma unroll
+  for (int u = 0; u < V / R0; ++u)
+#pragma unroll
+    for (int r = 0; r < R0; ++r) {
+      const int z = t + u * T + r * (L / R0);
+      const bool ok = r < R0 / 2 && z >= it.sz0 && z < it.sz1;
+#pragma unroll
+      for (int l = 0; l < 3; ++l) v[l][u * R0 + r] = ok ? col[l * cs + z * zs] : czero();
+    }
+  const int region = padded(L * W);
+  auto idx = [&](int l) { return SIdx{l * region, W, c}; };
+  fft_run<L, false, -1, 3>(v, sm, idx, t, p.tw_z, false);
+
+  // spectral 3x3 multiply with the packed (octant) Green spectrum and parity signs
+  const int ix = kx <= nx ? kx : Lx - kx;
+  const int iy = ky <= ny ? ky : Ly - ky;
+  const double sx = kx > nx ? -1.0 : 1.0, sy = ky > ny ? -1.0 : 1.0;
+  const long long gcs = (long long)(nz + 1) * (ny + 1) * (nx + 1);
+  const double2* g = p.ghat + (long long)iy * (nx + 1) + ix;
+  const long long gzs = (long long)(ny + 1) * (nx + 1);
+#pragma unroll
+  for (int u = 0; u < V / RF; ++u)
+#pragma unroll
+    for (int r = 0; r < RF; ++r) {
+      const int kz = t + u * T + r * (L / RF);
+      const int iz = kz <= nz ? kz : L - kz;
+      const double sz = kz > nz ? -1.0 : 1.0;
+      const double2* gz = g + iz * gzs;
+      const double2 gxx = ld2(gz), gyy = ld2(gz + gcs), gzz = ld2(gz + 2 * gcs);
+      const double2 gxy = cscale(ld2(gz + 3 * gcs), sx * sy);
+      const double2 gxz = cscale(ld2(gz + 4 * gcs), sx * sz);
+      const double2 gyz = cscale(ld2(gz + 5 * gcs), sy * sz);
+      const int s = u * RF + r;
+      const double2 j0 = v[0][s], j1 = v[1][s], j2 = v[2][s];
+      v[0][s] = cadd(cadd(cmul(gxx, j0), cmul(gxy, j1)), cmul(gxz, j2));
+      v[1][s] = cadd(cadd(cmul(gxy, j0), cmul(gyy, j1)), cmul(gyz, j2));
+      v[2][s] = cadd(cadd(cmul(gxz, j0), cmul(gyz, j1)), cmul(gzz, j2));
+    }
+  fft_run<L, true, +1, 3>(v, sm, idx, t, p.tw_zr, true);
+#pragma unroll
+  for (int u = 0; u < V / RBL; ++u)
+#pragma unroll
+    for (int r = 0; r < RBL / 2; ++r) {  // outputs z >= nz are discarded (crop)
+      const int z = t + u * T + r * (L / RBL);
+#pragma unroll
+      for (int l = 0; l < 3; ++l) col[l * cs + z * zs] = v[l][u * RBL + r];
+    }
+}
+
+// =====================================================================  K-D
+template <int L>
+__global__ void __launch_bounds__(512) k_yinv(const __grid_constant__ ApplyParams p) {
+  using P = FftPlan<L>;
+  constexpr int T = P::T, V = P::V, R0 = P::radix(0, false), RL = P::radix(P::NST - 1, false);
+  extern __shared__ double2 sm[];
+  const int W = blockDim.x / T;
+  const int c = threadIdx.x % W, t = threadIdx.x / W;
+  const int item = blockIdx.z / 3, q = blockIdx.z % 3;
+  const int Lx = 2 * p.nx;
+  const int kx = blockIdx.x * W + c;
+  const int z = blockIdx.y;
+  const double2* src = p.X2 + (((long long)item * 3 + q) * p.nz + z) * (long long)L * Lx + kx;
+  double2 v[1][V];
+#pragma unroll
+  for (int u = 0; u < V / R0; ++u)
+#pragma unroll
+    for (int r = 0; r < R0; ++r) v[0][u * R0 + r] = src[(long long)(t + u * T + r * (L / R0)) * Lx];
+  auto idx = [&](int) { return SIdx{0, W, c}; };
+  fft_run<L, false, +1, 1>(v, sm, idx, t, p.tw_y, false);
+  double2* dst = p.X1 + (((long long)item * 3 + q) * p.nz + z) * p.ny * Lx + kx;
+#pragma unroll
+  for (int u = 0; u < V / RL; ++u)
+#pragma unroll
+    for (int r = 0; r < RL / 2; ++r) dst[(long long)(t + u * T + r * (L / RL)) * Lx] = v[0][u * RL + r];
+}
+
+// =====================================================================  K-E
+template <int L>
+__global__ void __launch_bounds__(256) k_xinv(const __grid_constant__ ApplyParams p) {
+  using P = FftPlan<L>;
+  constexpr int T = P::T, V = P::V, R0 = P::radix(0, false), RL = P::radix(P::NST - 1, false);
+  extern __shared__ double2 sm[];
+  const ApplyItem& it = p.items[blockIdx.y];
+  const int rows_cta = blockDim.x / T;
+  const int lr = threadIdx.x / T, t = threadIdx.x % T;
+  const int nx = p.nx, ny = p.ny, nz = p.nz;
+  const int row = blockIdx.x * rows_cta + lr;
+  const bool valid = row < ny * nz;
+  const int yy = valid ? row % ny : 0, zz = valid ? row / ny : 0;
+  const long long N = (long long)nx * ny * nz;
+  double2 v[3][V];
+#pragma unroll
+  for (int l = 0; l < 3; ++l) {
+    const double2* src = p.X1 + ((((long long)blockIdx.y * 3 + l) * nz + zz) * ny + yy) * L;
+#pragma unroll
+    for (int u = 0; u < V / R0; ++u)
+#pragma unroll
+      for (int r = 0; r < R0; ++r) v[l][u * R0 + r] = valid ? src[t + u * T + r * (L / R0)] : czero();
+  }
+  const int region = padded(L);
+  auto idx = [&](int l) { return SIdx{(lr * 3 + l) * region, 1, 0}; };
+  fft_run<L, false, +1, 3>(v, sm, idx, t, p.tw_x, false);
+  if (!valid) return;
+  const long long off = ((long long)zz * ny + yy) * nx;
+  const double a = p.alpha * it.xscale, b = p.beta;
+#pragma unroll
+  for (int l = 0; l < 3; ++l) {
+    double2* yrow = it.y + l * N + off;
+    const double2* xrow = it.x + l * N + off;
+#pragma unroll
+    for (int u = 0; u < V / RL; ++u)
+#pragma unroll
+      for (int r = 0; r < RL / 2; ++r) {  // x >= nx discarded (crop)
+        const int x = t + u * T + r * (L / RL);
+        double2 o = cscale(v[l][u * RL + r], b);
+        if (a != 0.0) {
+          const double2 xi = ld2(xrow + x);
+          o.x = fma(a, xi.x, o.x);
+          o.y = fma(a, xi.y, o.y);
+        }
+        if (p.accumulate) o = cadd(o, yrow[x]);
+        yrow[x] = o;
+      }
+  }
+}
+
+// =====================================================================  host side
+// twiddle tables for every L = 2^p and both radix orders
+template <int L>
+static void fill_tw(std::vector<double2>& out, bool rev) {
+  using P = FftPlan<L>;
+  for (int s = 1; s < P::NST; ++s) {
+    const int R = P::radix(s, rev), Ns = P::ns(s, rev);
+    for (int r = 1; r < R; ++r)
+      for (int k = 0; k < Ns; ++k) {
+        // exp(-2 pi i r k / (Ns R)), argument reduced exactly in integers, long double trig
+        const long long m = (long long)r * k, M = (long long)Ns * R;
+        const long double ang = -2.0L * 3.14159265358979323846264338327950288L * (long double)m / (long double)M;
+        out.push_back(make_double2((double)cosl(ang), (double)sinl(ang)));
+      }
+  }
+}
+
+const double2* Twiddles::get(int L, int rev) const { return dev + off[ilog2i(L)][rev ? 1 : 0]; }
+
+ie_status build_twiddles(ie_ctx* c) {
+  std::vector<double2> h;
+  h.push_back(make_double2(1, 0));  // keep offsets of 1-stage plans valid
+  auto add = [&](int p, auto fn) {
+    for (int rev = 0; rev < 2; ++rev) {
+      c->tw.off[p][rev] = (int)h.size();
+      fn(h, rev != 0);
+      h.push_back(make_double2(1, 0));
+    }
+  };
+  add(1, fill_tw<2>);
+  add(2, fill_tw<4>);
+  add(3, fill_tw<8>);
+  add(4, fill_tw<16>);
+  add(5, fill_tw<32>);
+  add(6, fill_tw<64>);
+  add(7, fill_tw<128>);
+  add(8, fill_tw<256>);
+  add(9, fill_tw<512>);
+  add(10, fill_tw<1024>);
+  IE_CUDA(c, cudaMalloc(&c->tw.dev, h.size() * sizeof(double2)));
+  IE_CUDA(c, cudaMemcpy(c->tw.dev, h.data(), h.size() * sizeof(double2), cudaMemcpyHostToDevice));
+  return IE_OK;
+}
+
+size_t apply_scratch_bytes(int nx, int ny, int nz, int n_items) {
+  const size_t n = (size_t)nx * ny * nz;
+  return (size_t)n_items * 3 * (2 * n + 4 * n) * sizeof(double2);
+}
+
+// launch configuration -----------------------------------------------------------
+struct Cfg {
+  dim3 grid, block;
+  size_t smem;
+};
+
+template <int L>
+static int threads_per_line() {
+  return FftPlan<L>::T;
+}
+
+// opt in to > 48 KB dynamic shared memory (once per kernel instance and size)
+static cudaError_t prep(const void* kernel, size_t smem) {
+  static std::unordered_map<const void*, size_t> done;
+  if (smem <= 48 * 1024) return cudaSuccess;
+  auto f = done.find(kernel);
+  if (f != done.end() && f->second >= smem) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e == cudaSuccess) done[kernel] = smem;
+  return e;
+}
+
+// x-passes: rows_cta rows of 3 lines; y-passes: W columns; z-pass: W columns of 3 lines
+static int rows_per_cta(int T) { return T >= 128 ? 1 : 128 / T; }
+static int y_width(int T, int Lx) {
+  int W = 256 / T;
+  if (W < 8) W = (512 / T < 8) ? 512 / T : 8;  // <= 512 threads per CTA
+  if (W > Lx) W = Lx;
+  return W;
+}
+static int z_width(int L, int T, int Lx) {
+  int W = 8;
+  while (W > 1 && (size_t)3 * padded(L * W) * sizeof(double2) > 112 * 1024) W /= 2;
+  while (W * T < 128 && W * 2 <= Lx && (size_t)3 * padded(L * W * 2) * sizeof(double2) <= 112 * 1024) W *= 2;
+  if (W > Lx) W = Lx;
+  return W;
+}
+
+#define IE_DISPATCH_L(Lval, FN, ...)      \
+  switch (Lval) {                         \
+    case 2: FN<2>(__VA_ARGS__); break;     \
+    case 4: FN<4>(__VA_ARGS__); break;     \
+    case 8: FN<8>(__VA_ARGS__); break;     \
+    case 16: FN<16>(__VA_ARGS__); break;   \
+    case 32: FN<32>(__VA_ARGS__); break;   \
+    case 64: FN<64>(__VA_ARGS__); break;   \
+    case 128: FN<128>(__VA_ARGS__); break; \
+    case 256: FN<256>(__VA_ARGS__); break; \
+    case 512: FN<512>(__VA_ARGS__); break; \
+    case 1024: FN<1024>(__VA_ARGS__); break; \
+    default: return cudaErrorInvalidValue; \
+  }
+
+template <int L>
+static cudaError_t go_xfwd(const ApplyParams& p, cudaStream_t s, int max_rows) {
+  const int T = FftPlan<L>::T, rows = rows_per_cta(T);
+  const size_t smem = (size_t)rows * 3 * padded(L) * sizeof(double2);
+  cudaError_t e = prep((const void*)k_xfwd<L>, smem);
+  if (e) return e;
+  k_xfwd<L><<<dim3((max_rows + rows - 1) / rows, p.n_items), rows * T, smem, s>>>(p);
+  return cudaGetLastError();
+}
+template <int L>
+static cudaError_t go_yfwd(const ApplyParams& p, cudaStream_t s, int max_planes) {
+  const int T = FftPlan<L>::T, W = y_width(T, 2 * p.nx);
+  const size_t smem = (size_t)padded(L * W) * sizeof(double2);
+  cudaError_t e = prep((const void*)k_yfwd<L>, smem);
+  if (e) return e;
+  k_yfwd<L><<<dim3(2 * p.nx / W, max_planes, 3 * p.n_items), W * T, smem, s>>>(p);
+  return cudaGetLastError();
+}
+template <int L>
+static cudaError_t go_zconv(const ApplyParams& p, cudaStream_t s) {
+  const int T = FftPlan<L>::T, W = z_width(L, T, 2 * p.nx);
+  const size_t smem = (size_t)3 * padded(L * W) * sizeof(double2);
+  cudaError_t e = prep((const void*)k_zconv<L>, smem);
+  if (e) return e;
+  k_zconv<L><<<dim3(2 * p.nx / W, 2 * p.ny, p.n_items), W * T, smem, s>>>(p);
+  return cudaGetLastError();
+}
+template <int L>
+static cudaError_t go_yinv(const ApplyParams& p, cudaStream_t s) {
+  const int T = FftPlan<L>::T, W = y_width(T, 2 * p.nx);
+  const size_t smem = (size_t)padded(L * W) * sizeof(double2);
+  cudaError_t e = prep((const void*)k_yinv<L>, smem);
+  if (e) return e;
+  k_yinv<L><<<dim3(2 * p.nx / W, p.nz, 3 * p.n_items), W * T, smem, s>>>(p);
+  return cudaGetLastError();
+}
+template <int L>
+static cudaError_t go_xinv(const ApplyParams& p, cudaStream_t s) {
+  const int T = FftPlan<L>::T, rows = rows_per_cta(T);
+  const size_t smem = (size_t)rows * 3 * padded(L) * sizeof(double2);
+  cudaError_t e = prep((const void*)k_xinv<L>, smem);
+  if (e) return e;
+  k_xinv<L><<<dim3((p.ny * p.nz + rows - 1) / rows, p.n_items), rows * T, smem, s>>>(p);
+  return cudaGetLastError();
+}
+
+template <int L> static void wrap_xfwd(cudaError_t* e, const ApplyParams& p, cudaStream_t s, int m) { *e = go_xfwd<L>(p, s, m); }
+template <int L> static void wrap_yfwd(cudaError_t* e, const ApplyParams& p, cudaStream_t s, int m) { *e = go_yfwd<L>(p, s, m); }
+template <int L> static void wrap_zconv(cudaError_t* e, const ApplyParams& p, cudaStream_t s) { *e = go_zconv<L>(p, s); }
+template <int L> static void wrap_yinv(cudaError_t* e, const ApplyParams& p, cudaStream_t s) { *e = go_yinv<L>(p, s); }
+template <int L> static void wrap_xinv(cudaError_t* e, const ApplyParams& p, cudaStream_t s) { *e = go_xinv<L>(p, s); }
+
+static cudaError_t run_apply(const ApplyParams& p, cudaStream_t s) {
+  cudaError_t e = cudaSuccess;
+  int max_rows = 0, max_planes = 0;
+  for (int i = 0; i < p.n_items; ++i) {
+    const ApplyItem& it = p.items[i];
+    const int rows = (it.sy1 - it.sy0) * (it.sz1 - it.sz0);
+    if (rows > max_rows) max_rows = rows;
+    if (it.sz1 - it.sz0 > max_planes) max_planes = it.sz1 - it.sz0;
+  }
+  // items of one launch must share the source z range for K-B's plane indexing
+  IE_DISPATCH_L(2 * p.nx, wrap_xfwd, &e, p, s, max_rows);
+  if (e) return e;
+  IE_DISPATCH_L(2 * p.ny, wrap_yfwd, &e, p, s, max_planes);
+  if (e) return e;
+  IE_DISPATCH_L(2 * p.nz, wrap_zconv, &e, p, s);
+  if (e) return e;
+  IE_DISPATCH_L(2 * p.ny, wrap_yinv, &e, p, s);
+  if (e) return e;
+  IE_DISPATCH_L(2 * p.nx, wrap_xinv, &e, p, s);
+  return e;
+}
+
+ie_status launch_apply(ie_ctx* c, ApplyParams& p) {
+  if (p.n_items <= 0) return IE_OK;
+  if (p.n_items > kMaxItems) return fail(c, IE_ERR_INVALID_ARGUMENT, "internal: too many apply items");
+  for (int i = 1; i < p.n_items; ++i)
+    if (p.items[i].sz0 != p.items[0].sz0 || p.items[i].sz1 != p.items[0].sz1 ||
+        p.items[i].sy0 != p.items[0].sy0 || p.items[i].sy1 != p.items[0].sy1)
+      return fail(c, IE_ERR_INVALID_ARGUMENT, "internal: batched apply items must share the source y/z range");
+  p.tw_x = c->tw.get(2 * p.nx, 0);
+  p.tw_y = c->tw.get(2 * p.ny, 0);
+  p.tw_z = c->tw.get(2 * p.nz, 0);
+  p.tw_zr = c->tw.get(2 * p.nz, 1);
+  cudaError_t e = run_apply(p, c->stream);
+  c->launches += 5;
+  if (e != cudaSuccess) return cuda_fail(c, e, "operator kernels");
+  return IE_OK;
+}
+
+}  // namespace ie

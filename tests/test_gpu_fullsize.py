@@ -1,0 +1,49 @@
+"""Parity at BASELINE.json's full sizes, in the launch configuration bench.py times: the
+operator on the c5 (256x256x128) and c4h (128x128x64) grids, sampled output cells checked
+against the oracle's direct summation of Eq. 3 (one output cell at a time), plus
+properties that hold at any size (linearity, zero contrast)."""
+
+import numpy as np
+import pytest
+
+from ie_workloads import make_config
+from oracle import physics, operator as op
+from gpu_helpers import gpu_ctx, rel
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("name", ["c5", "c4h"])
+def test_fullsize_operator_sampled_cells(name):
+    import torch
+    import paper_2306_17537_b200 as ie
+    cfg = make_config(name)
+    sigma = cfg.sigma()
+    ctx, _ = gpu_ctx(cfg, sigma=sigma, boxes=[], nrhs=1, restart=2)
+    nx, ny, nz = cfg.n
+    e0 = torch.empty((len(cfg.sources), 3, nz, ny, nx), dtype=torch.complex128, device="cuda")
+    ie.ie_get_incident(ctx, e0)
+    x = e0[:1].contiguous()
+    y = torch.empty_like(x)
+    ie.ie_apply_operator(ctx, x, y)
+    torch.cuda.synchronize()
+    xh = x.cpu().numpy()[0]
+    yh = y.cpu().numpy()[0]
+    k0 = physics.wavenumber(cfg.sigma_b, cfg.freq)
+    ds = physics.contrast(sigma, cfg.sigma_b)
+    rng = np.random.default_rng(0)
+    cells = [(0, 0, 0), (nx - 1, ny - 1, nz - 1), (nx // 2, ny // 2, nz // 2)]
+    cells += [tuple(int(v) for v in rng.integers(0, [nx, ny, nz])) for _ in range(2)]
+    ref = op.direct_rows(cfg.n, cfg.hvec, k0, cfg.sigma_b, ds, xh, cells)
+    scale = np.abs(yh).max()
+    for t, (cx, cy, cz) in enumerate(cells):
+        got = yh[:, cz, cy, cx]
+        assert np.abs(got - ref[t]).max() < 1e-11 * scale, (cells[t], got, ref[t])
+    # linearity at full size: A(a x + b z) = a A x + b A z
+    z = torch.roll(x, shifts=3, dims=4) * (0.5 - 0.25j)
+    w = torch.empty_like(x)
+    ie.ie_apply_operator(ctx, (2.0 + 1j) * x + z, w)
+    v = torch.empty_like(x)
+    ie.ie_apply_operator(ctx, z, v)
+    lin = (2.0 + 1j) * y + v
+    assert float(torch.linalg.vector_norm(w - lin) / torch.linalg.vector_norm(lin)) < 1e-13

@@ -1,0 +1,133 @@
+"""GPU parity of the operator path (A0 Green spectrum, A1-A5 operator, A7 box operator,
+A10 incident field) against the CPU oracle, element by element.  Tolerance: relative L2
+<= 1e-12 in complex128 (BASELINE.json north_star)."""
+
+import numpy as np
+import pytest
+
+from ie_workloads import Config, make_config
+from oracle import physics, operator as op
+from gpu_helpers import gpu_ctx, oracle_setup, rel
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-12
+
+
+def _rand_sigma(rng, cfg, aniso=True, scale=1.0):
+    nx, ny, nz = cfg.n
+    A = rng.standard_normal((nz, ny, nx, 3, 3)) * 0.3 * scale
+    S = 0.5 * (A + np.swapaxes(A, -1, -2)) if aniso else np.eye(3) * A[..., :1, :1]
+    return S + cfg.sigma_b * np.eye(3)
+
+
+def _cfg(n, h=0.2, sigma_b=0.3, freq=4e5):
+    return Config("custom", n, h, sigma_b, freq, 0, None, sources=[(np.array([0.013, 0.021, 0.017]) + 0.0,
+                                                                     np.array([0.2, -0.3, 1.0]))])
+
+
+SHAPES = [(8, 8, 8), (16, 8, 4), (4, 16, 32), (1, 2, 4), (2, 1, 1), (32, 4, 2), (64, 8, 16), (8, 64, 2),
+          (2, 2, 128), (128, 2, 2), (512, 1, 2)]
+
+
+@pytest.mark.parametrize("n", SHAPES)
+def test_green_octant_matches_oracle_spectrum(n):
+    import paper_2306_17537_b200 as ie
+    cfg = _cfg(n)
+    rng = np.random.default_rng(1)
+    ctx, sigma = gpu_ctx(cfg, sigma=_rand_sigma(rng, cfg), boxes=[], restart=2)
+    k0 = physics.wavenumber(cfg.sigma_b, cfg.freq)
+    Gh = op.green_spectra(cfg.n, cfg.hvec, k0, cfg.sigma_b) / (8 * np.prod(n))
+    nx, ny, nz = n
+    oct_gpu = ie.ie_get_green_octant(ctx)
+    comps = [(0, 0), (1, 1), (2, 2), (0, 1), (0, 2), (1, 2)]
+    for c, (p, q) in enumerate(comps):
+        ref = Gh[p, q][:nz + 1, :ny + 1, :nx + 1]
+        assert rel(oct_gpu[c], ref) < TOL, (c, rel(oct_gpu[c], ref))
+    info = ie.ie_get_info(ctx)
+    assert abs(info["k0"] - k0) < 1e-15 * abs(k0)
+    K0 = physics.self_term(k0, cfg.sigma_b, cfg.h ** 3)[0, 0]
+    assert abs(info["self_term"] - K0) < 1e-14 * abs(K0)
+
+
+@pytest.mark.parametrize("n", SHAPES)
+@pytest.mark.parametrize("nrhs", [1, 3])
+def test_apply_operator_matches_oracle(n, nrhs):
+    import torch
+    import paper_2306_17537_b200 as ie
+    cfg = _cfg(n)
+    rng = np.random.default_rng(2)
+    ctx, sigma = gpu_ctx(cfg, sigma=_rand_sigma(rng, cfg), boxes=[], nrhs=nrhs, restart=2)
+    nx, ny, nz = n
+    x = rng.standard_normal((nrhs, 3, nz, ny, nx)) + 1j * rng.standard_normal((nrhs, 3, nz, ny, nx))
+    xd = torch.from_numpy(x).cuda()
+    yd = torch.full_like(xd, np.nan)
+    ie.ie_apply_operator(ctx, xd, yd)
+    k0, ds, _ = oracle_setup(cfg, sigma)
+    A = op.Operator(cfg.n, cfg.hvec, k0, cfg.sigma_b, ds)
+    y = yd.cpu().numpy()
+    for r in range(nrhs):
+        assert rel(y[r], A(x[r])) < TOL
+
+
+def test_apply_zero_contrast_is_identity_bitwise():
+    import torch
+    import paper_2306_17537_b200 as ie
+    cfg = _cfg((16, 8, 32))
+    sig = np.zeros((32, 8, 16, 3, 3)) + cfg.sigma_b * np.eye(3)
+    ctx, _ = gpu_ctx(cfg, sigma=sig, boxes=[], restart=2)
+    rng = np.random.default_rng(3)
+    x = rng.standard_normal((1, 3, 32, 8, 16)) + 1j * rng.standard_normal((1, 3, 32, 8, 16))
+    xd = torch.from_numpy(x).cuda()
+    yd = torch.empty_like(xd)
+    ie.ie_apply_operator(ctx, xd, yd)
+    assert np.array_equal(yd.cpu().numpy(), x)
+
+
+@pytest.mark.parametrize("box", [(0, 8, 0, 8, 0, 4), (8, 16, 0, 4, 4, 8), (2, 4, 1, 2, 7, 8), (0, 16, 0, 8, 0, 8)])
+def test_apply_on_box_is_the_diagonal_block(box):
+    """y = (I - G^(ii) dsigma^(i)) x on a box = the restriction of Eq. 8 to that box (Eq. 15)."""
+    import torch
+    import paper_2306_17537_b200 as ie
+    cfg = _cfg((16, 8, 8))
+    rng = np.random.default_rng(4)
+    ctx, sigma = gpu_ctx(cfg, sigma=_rand_sigma(rng, cfg), boxes=[box], restart=2)
+    i0, i1, j0, j1, k0_, k1 = box
+    bn = (i1 - i0, j1 - j0, k1 - k0_)
+    x = rng.standard_normal((1, 3, bn[2], bn[1], bn[0])) + 1j * rng.standard_normal((1, 3, bn[2], bn[1], bn[0]))
+    xd = torch.from_numpy(x).cuda()
+    yd = torch.empty_like(xd)
+    ie.ie_apply_operator(ctx, xd, yd, box=box)
+    k0, ds, _ = oracle_setup(cfg, sigma)
+    A = op.Operator(bn, cfg.hvec, k0, cfg.sigma_b, ds[k0_:k1, j0:j1, i0:i1])
+    assert rel(yd.cpu().numpy()[0], A(x[0])) < TOL
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c3mini", "c5mini"])
+def test_incident_field_matches_oracle(name):
+    import torch
+    import paper_2306_17537_b200 as ie
+    cfg = make_config(name)
+    ctx, sigma = gpu_ctx(cfg, boxes=[], restart=2)
+    nx, ny, nz = cfg.n
+    e0 = torch.empty((len(cfg.sources), 3, nz, ny, nx), dtype=torch.complex128, device="cuda")
+    ie.ie_get_incident(ctx, e0)
+    _, _, E0 = oracle_setup(cfg, sigma)
+    assert rel(e0.cpu().numpy(), E0) < TOL
+
+
+def test_source_on_centroid_is_rejected():
+    import paper_2306_17537_b200 as ie
+    cfg = make_config("c1")
+    ctx, _ = gpu_ctx(cfg, boxes=[], restart=2)
+    with pytest.raises(ie.IEError) as e:
+        ie.ie_set_source(ctx, np.array([cfg.origin]), np.array([[0, 0, 1.0]]))
+    assert e.value.status == 7
+
+
+def test_invalid_arguments_fail_loudly():
+    import paper_2306_17537_b200 as ie
+    with pytest.raises(ie.IEError) as e:
+        ie.ie_create((6, 8, 8), (0.1, 0.1, 0.1), (0, 0, 0), 1.0, 1e5)
+    assert e.value.status == 1
+    with pytest.raises(ie.IEError):
+        ie.ie_create((8, 8, 8), (0.1, 0.1, 0.1), (0, 0, 0), -1.0, 1e5)
