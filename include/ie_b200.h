@@ -203,6 +203,13 @@ typedef struct {
   int32_t kernel_launches; /* number of CUDA kernel launches issued by this context so far */
 } ie_info;
 ie_status ie_get_info(const ie_ctx* ctx, ie_info* info);
+/* Per-kernel device timing of the operator (benchmarks).  enable != 0 starts recording CUDA
+ * events around each of the five operator kernels (K-A x-forward+contrast, K-B y-forward,
+ * K-C z-convolution, K-D y-inverse, K-E x-inverse+update) on the context stream; enable = 0
+ * stops and clears.  ie_profile_read synchronises the stream and returns, for each kernel k,
+ * the summed device time ms[k] (milliseconds) and the number of launches counts[k]. */
+ie_status ie_profile(ie_ctx* ctx, int32_t enable);
+ie_status ie_profile_read(ie_ctx* ctx, double* ms /*[5]*/, int32_t* counts /*[5]*/);
 /* Copy the packed Green spectrum of the given box shape (box = NULL: the grid) to the host:
  * complex128 [6][bz+1][by+1][bx+1], components (xx, yy, zz, xy, xz, yz), scaled by
  * 1/(8 bx by bz); entry (kx,ky,kz) of the full padded spectrum F[G_pq] (Eq. 10) is

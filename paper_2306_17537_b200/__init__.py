@@ -26,7 +26,10 @@ SCHEMES = {"full": IE_DD_FULL, "jacobi": IE_DD_JACOBI, "gauss_seidel": IE_DD_GAU
 
 EXPORTED = ("ie_create", "ie_destroy", "ie_last_error", "ie_workspace_query", "ie_bind_workspace",
             "ie_set_contrast", "ie_set_source", "ie_get_incident", "ie_set_incident", "ie_apply_operator",
-            "ie_solve_subdomain", "ie_solve_dd", "ie_receiver_fields", "ie_get_info", "ie_get_green_octant")
+            "ie_solve_subdomain", "ie_solve_dd", "ie_receiver_fields", "ie_get_info", "ie_get_green_octant",
+            "ie_profile", "ie_profile_read")
+KERNELS = ("K-A x-forward+contrast", "K-B y-forward", "K-C z-convolution", "K-D y-inverse",
+           "K-E x-inverse+update")
 
 
 class IEError(RuntimeError):
@@ -106,6 +109,8 @@ def load_library(path=LIB_PATH):
         "ie_receiver_fields": [P, P, I, P, P, P],
         "ie_get_info": [P, ctypes.POINTER(ie_info)],
         "ie_get_green_octant": [P, ctypes.POINTER(ie_box), P],
+        "ie_profile": [P, I],
+        "ie_profile_read": [P, P, P],
     }
     for name, args in sig.items():
         f = getattr(lib, name)
@@ -298,3 +303,15 @@ def ie_get_green_octant(ctx, box=None):
     out = np.zeros((6, nz + 1, ny + 1, nx + 1), np.complex128)
     _check(ctx, _lib.ie_get_green_octant(ctx.handle, _box(box), _ptr(out)), "ie_get_green_octant")
     return out
+
+
+def ie_profile(ctx, enable=True):
+    _check(ctx, _lib.ie_profile(ctx.handle, int(bool(enable))), "ie_profile")
+
+
+def ie_profile_read(ctx):
+    """Returns {kernel name: (total ms, launches)} for the operator kernels since ie_profile(ctx, True)."""
+    ms = np.zeros(5, np.float64)
+    cnt = np.zeros(5, np.int32)
+    _check(ctx, _lib.ie_profile_read(ctx.handle, _ptr(ms), _ptr(cnt)), "ie_profile_read")
+    return {k: (float(ms[i]), int(cnt[i])) for i, k in enumerate(KERNELS)}

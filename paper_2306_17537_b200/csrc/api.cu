@@ -190,6 +190,7 @@ ie_status ie_destroy(ie_ctx* c) {
   cudaFree(c->tw.dev);
   cudaFree(c->d_red);
   if (c->h_red) cudaFreeHost(c->h_red);
+  for (auto ev : c->ev_pool) cudaEventDestroy(ev);
   delete c;
   return IE_OK;
 }
@@ -592,6 +593,31 @@ ie_status ie_get_info(const ie_ctx* c, ie_info* info) {
   info->self_im = c->self.imag();
   info->n_src = c->n_src;
   info->kernel_launches = (int32_t)std::min<long long>(c->launches, 0x7fffffff);
+  return IE_OK;
+}
+
+ie_status ie_profile(ie_ctx* c, int32_t enable) {
+  if (!c) return IE_ERR_INVALID_ARGUMENT;
+  c->profiling = enable != 0;
+  c->ev_marks.clear();
+  c->ev_used = 0;
+  return IE_OK;
+}
+
+ie_status ie_profile_read(ie_ctx* c, double* ms, int32_t* counts) {
+  if (!c || !ms || !counts) return fail(c, IE_ERR_INVALID_ARGUMENT, "profile_read: bad arguments");
+  IE_CUDA(c, cudaStreamSynchronize(c->stream));
+  for (int k = 0; k < 5; ++k) {
+    ms[k] = 0;
+    counts[k] = 0;
+  }
+  for (auto& mk : c->ev_marks)
+    for (int k = 0; k < 5; ++k) {
+      float t = 0;
+      IE_CUDA(c, cudaEventElapsedTime(&t, c->ev_pool[mk.second + k], c->ev_pool[mk.second + k + 1]));
+      ms[k] += t;
+      counts[k] += 1;
+    }
   return IE_OK;
 }
 

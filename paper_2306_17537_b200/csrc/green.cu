@@ -89,8 +89,9 @@ __global__ void __launch_bounds__(512) k_fft_axis(double2* __restrict__ data, lo
   extern __shared__ double2 sm[];
   const int lpc = blockDim.x / (T * W);
   const int c = threadIdx.x % W, t = (threadIdx.x / W) % T, lo = threadIdx.x / (W * T);
-  const long long line = (long long)blockIdx.y * lpc + lo;
-  const long long col = (long long)blockIdx.x * W + c;
+  const long long ncb = (inner + W - 1) / W;  // column blocks; flattened grid (x dim holds 2^31)
+  const long long line = (long long)(blockIdx.x / ncb) * lpc + lo;
+  const long long col = (long long)(blockIdx.x % ncb) * W + c;
   const bool valid = line < outer && col < inner;
   double2* base = data + line * L * inner + col;
   double2 v[1][V];
@@ -135,7 +136,7 @@ static cudaError_t fft_axis_launch(double2* data, long long inner, long long out
                                          (int)smem);
     if (e) return e;
   }
-  dim3 grid((unsigned)((inner + W - 1) / W), (unsigned)((outer + lpc - 1) / lpc));
+  dim3 grid((unsigned)(((inner + W - 1) / W) * ((outer + lpc - 1) / lpc)));
   k_fft_axis<L><<<grid, lpc * T * W, smem, s>>>(data, inner, outer, tw, W);
   return cudaGetLastError();
 }

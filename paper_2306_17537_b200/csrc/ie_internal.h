@@ -91,6 +91,11 @@ struct ie_ctx {
   size_t h_red_cap = 0;
   double2* d_red = nullptr;  // device mirror for coefficient uploads
   size_t d_red_cap = 0;
+  // per-kernel profiling of the operator (ie_profile): events[i] brackets kernel kind[i]
+  bool profiling = false;
+  std::vector<cudaEvent_t> ev_pool;
+  std::vector<std::pair<int, int>> ev_marks;  // (kernel id, index of the start event)
+  size_t ev_used = 0;
 };
 
 namespace ie {

@@ -122,10 +122,13 @@ void* Arena::take(size_t bytes) {
   return base + a;
 }
 
+// CTAs per system for the multi-dot kernel: ~2368 CTAs in total (16 per SM)
+static int dot_blocks(int nsys) { return std::max(32, std::min(1184, 2368 / std::max(1, nsys))); }
+
 size_t gmres_scratch_bytes(int nx, int ny, int nz, int nsys, int restart) {
   const size_t len = 3ull * nx * ny * nz;
   const int items = std::min(nsys, kMaxItems);
-  const int nblk = 64;
+  const int nblk = dot_blocks(nsys);
   size_t b = 0;
   auto add = [&](size_t x) { b = ((b + 255) & ~(size_t)255) + x; };
   add((size_t)nsys * (restart + 1) * len * sizeof(double2));           // V
@@ -159,7 +162,7 @@ ie_status gmres_batched(ie_ctx* c, Arena& ar, int nx, int ny, int nz, long long 
   if (S == 0) return IE_OK;
   const long long N = (long long)nx * ny * nz, len = 3 * N;
   const int items = std::min(S, kMaxItems);
-  const int nblk = 64;
+  const int nblk = dot_blocks(S);
   ie_status st;
   const GreenSpec* gs = green_for(c, nx, ny, nz, &st);
   if (!gs) return st;

@@ -129,54 +129,80 @@ __global__ void __launch_bounds__(256) k_zconv(const __grid_constant__ ApplyPara
   double2* col = p.X2 + (long long)item * 3 * cs + (long long)ky * Lx + kx;
   const long long zs = (long long)Ly * Lx;
 
-  double2 v[3][V];
+  // all (pruned) inputs of the 3 components first: 3*V/2 independent loads in flight
+  double2 in[3][V / 2];
 #pragma unroll
   for (int u = 0; u < V / R0; ++u)
 #pragma unroll
-    for (int r = 0; r < R0; ++r) {
+    for (int r = 0; r < R0 / 2; ++r) {  // r >= R0/2 <=> z >= nz: zero padding
       const int z = t + u * T + r * (L / R0);
-      const bool ok = r < R0 / 2 && z >= it.sz0 && z < it.sz1;
+      const bool ok = z >= it.sz0 && z < it.sz1;
 #pragma unroll
-      for (int l = 0; l < 3; ++l) v[l][u * R0 + r] = ok ? col[l * cs + z * zs] : czero();
+      for (int l = 0; l < 3; ++l) in[l][u * (R0 / 2) + r] = ok ? col[l * cs + z * zs] : czero();
     }
   const int region = padded(L * W);
-  auto idx = [&](int l) { return SIdx{l * region, W, c}; };
-  fft_run<L, false, -1, 3>(v, sm, idx, t, p.tw_z, false);
+  // forward z-FFTs one component at a time (8 live values per thread); each spectrum is
+  // parked in this thread's own slots of its region
+#pragma unroll
+  for (int l = 0; l < 3; ++l) {
+    double2 v[1][V];
+#pragma unroll
+    for (int u = 0; u < V / R0; ++u)
+#pragma unroll
+      for (int r = 0; r < R0; ++r) v[0][u * R0 + r] = (r < R0 / 2) ? in[l][u * (R0 / 2) + r] : czero();
+    auto idx = [&](int) { return SIdx{l * region, W, c}; };
+    fft_run<L, false, -1, 1>(v, sm, idx, t, p.tw_z, false);
+    if constexpr (P::NST > 1) __syncthreads();  // the last stage read other threads' slots
+#pragma unroll
+    for (int u = 0; u < V / RF; ++u)
+#pragma unroll
+      for (int r = 0; r < RF; ++r) sm[idx(0)(t + u * T + r * (L / RF))] = v[0][u * RF + r];
+  }
 
-  // spectral 3x3 multiply with the packed (octant) Green spectrum and parity signs
+  // spectral 3x3 multiply with the packed (octant) Green spectrum and parity signs, one kz
+  // at a time on this thread's own slots
   const int ix = kx <= nx ? kx : Lx - kx;
   const int iy = ky <= ny ? ky : Ly - ky;
   const double sx = kx > nx ? -1.0 : 1.0, sy = ky > ny ? -1.0 : 1.0;
   const long long gcs = (long long)(nz + 1) * (ny + 1) * (nx + 1);
   const double2* g = p.ghat + (long long)iy * (nx + 1) + ix;
   const long long gzs = (long long)(ny + 1) * (nx + 1);
+  auto sidx = [&](int l, int i) { return SIdx{l * region, W, c}(i); };
+#pragma unroll 2
+  for (int s = 0; s < V; ++s) {
+    const int kz = t + (s / RF) * T + (s % RF) * (L / RF);
+    const int iz = kz <= nz ? kz : L - kz;
+    const double sz = kz > nz ? -1.0 : 1.0;
+    const double2* gz = g + iz * gzs;
+    const double2 gxx = ld2(gz), gyy = ld2(gz + gcs), gzz = ld2(gz + 2 * gcs);
+    const double2 gxy = cscale(ld2(gz + 3 * gcs), sx * sy);
+    const double2 gxz = cscale(ld2(gz + 4 * gcs), sx * sz);
+    const double2 gyz = cscale(ld2(gz + 5 * gcs), sy * sz);
+    const int i0 = sidx(0, kz), i1 = sidx(1, kz), i2 = sidx(2, kz);
+    const double2 j0 = sm[i0], j1 = sm[i1], j2 = sm[i2];
+    sm[i0] = cadd(cadd(cmul(gxx, j0), cmul(gxy, j1)), cmul(gxz, j2));
+    sm[i1] = cadd(cadd(cmul(gxy, j0), cmul(gyy, j1)), cmul(gyz, j2));
+    sm[i2] = cadd(cadd(cmul(gxz, j0), cmul(gyz, j1)), cmul(gzz, j2));
+  }
+
+  // inverse z-FFTs (order B starts on the positions order F ended on), crop to z < nz
 #pragma unroll
-  for (int u = 0; u < V / RF; ++u)
+  for (int l = 0; l < 3; ++l) {
+    double2 v[1][V];
+    auto idx = [&](int) { return SIdx{l * region, W, c}; };
 #pragma unroll
-    for (int r = 0; r < RF; ++r) {
-      const int kz = t + u * T + r * (L / RF);
-      const int iz = kz <= nz ? kz : L - kz;
-      const double sz = kz > nz ? -1.0 : 1.0;
-      const double2* gz = g + iz * gzs;
-      const double2 gxx = ld2(gz), gyy = ld2(gz + gcs), gzz = ld2(gz + 2 * gcs);
-      const double2 gxy = cscale(ld2(gz + 3 * gcs), sx * sy);
-      const double2 gxz = cscale(ld2(gz + 4 * gcs), sx * sz);
-      const double2 gyz = cscale(ld2(gz + 5 * gcs), sy * sz);
-      const int s = u * RF + r;
-      const double2 j0 = v[0][s], j1 = v[1][s], j2 = v[2][s];
-      v[0][s] = cadd(cadd(cmul(gxx, j0), cmul(gxy, j1)), cmul(gxz, j2));
-      v[1][s] = cadd(cadd(cmul(gxy, j0), cmul(gyy, j1)), cmul(gyz, j2));
-      v[2][s] = cadd(cadd(cmul(gxz, j0), cmul(gyz, j1)), cmul(gzz, j2));
-    }
-  fft_run<L, true, +1, 3>(v, sm, idx, t, p.tw_zr, true);
+    for (int u = 0; u < V / RF; ++u)
 #pragma unroll
-  for (int u = 0; u < V / RBL; ++u)
+      for (int r = 0; r < RF; ++r) v[0][u * RF + r] = sm[idx(0)(t + u * T + r * (L / RF))];
+    fft_run<L, true, +1, 1>(v, sm, idx, t, p.tw_zr, true);
 #pragma unroll
-    for (int r = 0; r < RBL / 2; ++r) {  // outputs z >= nz are discarded (crop)
-      const int z = t + u * T + r * (L / RBL);
+    for (int u = 0; u < V / RBL; ++u)
 #pragma unroll
-      for (int l = 0; l < 3; ++l) col[l * cs + z * zs] = v[l][u * RBL + r];
-    }
+      for (int r = 0; r < RBL / 2; ++r) {  // outputs z >= nz are discarded (crop)
+        const int z = t + u * T + r * (L / RBL);
+        col[l * cs + z * zs] = v[0][u * RBL + r];
+      }
+  }
 }
 
 // =====================================================================  K-D
@@ -410,7 +436,7 @@ template <int L> static void wrap_zconv(cudaError_t* e, const ApplyParams& p, cu
 template <int L> static void wrap_yinv(cudaError_t* e, const ApplyParams& p, cudaStream_t s) { *e = go_yinv<L>(p, s); }
 template <int L> static void wrap_xinv(cudaError_t* e, const ApplyParams& p, cudaStream_t s) { *e = go_xinv<L>(p, s); }
 
-static cudaError_t run_apply(const ApplyParams& p, cudaStream_t s) {
+static cudaError_t run_apply(const ApplyParams& p, cudaStream_t s, cudaEvent_t* ev) {
   cudaError_t e = cudaSuccess;
   int max_rows = 0, max_planes = 0;
   for (int i = 0; i < p.n_items; ++i) {
@@ -419,16 +445,25 @@ static cudaError_t run_apply(const ApplyParams& p, cudaStream_t s) {
     if (rows > max_rows) max_rows = rows;
     if (it.sz1 - it.sz0 > max_planes) max_planes = it.sz1 - it.sz0;
   }
-  // items of one launch must share the source z range for K-B's plane indexing
+  auto mark = [&](int k) {
+    if (ev) cudaEventRecord(ev[k], s);
+  };
+  // items of one launch share the source y/z range (K-A rows, K-B planes)
+  mark(0);
   IE_DISPATCH_L(2 * p.nx, wrap_xfwd, &e, p, s, max_rows);
   if (e) return e;
+  mark(1);
   IE_DISPATCH_L(2 * p.ny, wrap_yfwd, &e, p, s, max_planes);
   if (e) return e;
+  mark(2);
   IE_DISPATCH_L(2 * p.nz, wrap_zconv, &e, p, s);
   if (e) return e;
+  mark(3);
   IE_DISPATCH_L(2 * p.ny, wrap_yinv, &e, p, s);
   if (e) return e;
+  mark(4);
   IE_DISPATCH_L(2 * p.nx, wrap_xinv, &e, p, s);
+  mark(5);
   return e;
 }
 
@@ -443,7 +478,18 @@ ie_status launch_apply(ie_ctx* c, ApplyParams& p) {
   p.tw_y = c->tw.get(2 * p.ny, 0);
   p.tw_z = c->tw.get(2 * p.nz, 0);
   p.tw_zr = c->tw.get(2 * p.nz, 1);
-  cudaError_t e = run_apply(p, c->stream);
+  cudaEvent_t* ev = nullptr;
+  if (c->profiling) {
+    while (c->ev_pool.size() < c->ev_used + 6) {
+      cudaEvent_t x;
+      IE_CUDA(c, cudaEventCreate(&x));
+      c->ev_pool.push_back(x);
+    }
+    ev = &c->ev_pool[c->ev_used];
+    c->ev_marks.push_back({0, (int)c->ev_used});
+    c->ev_used += 6;
+  }
+  cudaError_t e = run_apply(p, c->stream, ev);
   c->launches += 5;
   if (e != cudaSuccess) return cuda_fail(c, e, "operator kernels");
   return IE_OK;

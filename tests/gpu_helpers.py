@@ -24,13 +24,16 @@ def oracle_setup(cfg, sigma):
     k0 = physics.wavenumber(cfg.sigma_b, cfg.freq)
     ds = physics.contrast(sigma, cfg.sigma_b)
     pts = physics.centroids(cfg.n, cfg.hvec, cfg.origin)
-    E0 = np.stack([np.moveaxis(physics.incident_E(pts, s, m, k0, cfg.freq), -1, 0) for s, m in cfg.sources]) \
-        if cfg.sources else None
+    E0 = np.ascontiguousarray(np.stack([np.moveaxis(physics.incident_E(pts, s, m, k0, cfg.freq), -1, 0)
+                                        for s, m in cfg.sources])) if cfg.sources else None
     return k0, ds, E0
 
 
 def rel(a, b):
-    return float(np.linalg.norm((a - b).ravel()) / np.linalg.norm(b.ravel()))
+    """Relative L2 error; for an all-zero reference the absolute L2 norm of a (must be 0-ish)."""
+    nb = np.linalg.norm(np.asarray(b).ravel())
+    d = np.linalg.norm((np.asarray(a) - np.asarray(b)).ravel())
+    return float(d / nb) if nb > 0 else float(d)
 
 
 __all__ = ["gpu_ctx", "oracle_setup", "rel", "make_config"]
