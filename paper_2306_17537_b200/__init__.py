@@ -148,6 +148,10 @@ class IECtx:
         self.workspace = None
         self.n_src = 0
 
+    def last_error(self):
+        msg = _lib.ie_last_error(self.handle) if _lib is not None else None
+        return msg.decode() if msg else ""
+
     def __del__(self):
         try:
             if self.handle and _lib is not None:

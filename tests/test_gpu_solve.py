@@ -100,7 +100,7 @@ def test_dd_gs_single_sweep_matches_oracle_forward_substitution():
     from oracle import dd
     cfg = make_config("c2mini")
     boxes = [(0, 8, 0, 8, 0, 2), (0, 8, 0, 8, 2, 4), (0, 8, 0, 8, 4, 8)]
-    ctx, sigma = gpu_ctx(cfg, boxes=boxes)
+    ctx, sigma = gpu_ctx(cfg, boxes=boxes, restart=60)  # workspace sized for the restart used below
     k0, ds, E0, _ = _lu_truth(cfg, sigma)
     A = op.dense_matrix(cfg.n, cfg.hvec, k0, cfg.sigma_b, ds)
     blocks, ids = dd.dense_blocks(A, cfg.n, boxes)
@@ -108,7 +108,7 @@ def test_dd_gs_single_sweep_matches_oracle_forward_substitution():
     e = _field(cfg, 1)
     st = ie.ie_solve_dd(ctx, e, "gauss_seidel", boxes=boxes, outer_tol=1e-30, adaptive=False,
                         inner_tol_fixed=1e-13, max_sweeps=1, restart=60, check=False)
-    assert st["sweeps"] == 1
+    assert st["status"] == 0 and st["sweeps"] == 1, (ie.STATUS.get(st["status"]), ctx.last_error())
     got = e.cpu().numpy()[0].ravel()
     for b in range(3):
         assert np.linalg.norm(got[ids[b]] - ref[b]) < 1e-10 * np.linalg.norm(E0)
