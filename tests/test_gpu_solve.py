@@ -108,7 +108,9 @@ def test_dd_gs_single_sweep_matches_oracle_forward_substitution():
     e = _field(cfg, 1)
     st = ie.ie_solve_dd(ctx, e, "gauss_seidel", boxes=boxes, outer_tol=1e-30, adaptive=False,
                         inner_tol_fixed=1e-13, max_sweeps=1, restart=60, check=False)
-    assert st["status"] == 0 and st["sweeps"] == 1, (ie.STATUS.get(st["status"]), ctx.last_error())
+    # outer_tol 1e-30 is out of reach, so stopping at max_sweeps=1 reports NOT_CONVERGED (R16)
+    assert ie.STATUS[st["status"]] == "IE_ERR_NOT_CONVERGED" and st["sweeps"] == 1, (ie.STATUS.get(st["status"]),
+                                                                           ctx.last_error())
     got = e.cpu().numpy()[0].ravel()
     for b in range(3):
         assert np.linalg.norm(got[ids[b]] - ref[b]) < 1e-10 * np.linalg.norm(E0)
