@@ -86,11 +86,71 @@ __device__ __forceinline__ void dft8(double2* v) {
   v[3] = cadd(e3, o3);
   v[7] = csub(e3, o3);
 }
+// multiply by w16 = exp(DIR i pi/8) and w16^3 = exp(3 DIR i pi/8)
+template <int DIR>
+__device__ __forceinline__ double2 mul_w16(double2 a) {
+  constexpr double c = 0.92387953251128675612818318939678829, s = DIR * 0.38268343236508977172845998403039887;
+  return make_double2(fma(a.x, c, -a.y * s), fma(a.x, s, a.y * c));
+}
+template <int DIR>
+__device__ __forceinline__ double2 mul_w163(double2 a) {
+  constexpr double c = 0.38268343236508977172845998403039887, s = DIR * 0.92387953251128675612818318939678829;
+  return make_double2(fma(a.x, c, -a.y * s), fma(a.x, s, a.y * c));
+}
+
+// 16-point DFT, natural order, as 4 x 4 (n = 4 n1 + n2, k = k1 + 4 k2).
+// HALF_IN: v[8..15] are zero and not read (the zero-padded upper half of a forward pass);
+// HALF_OUT: only X[0..7] are produced (the cropped lower half of an inverse pass).
+template <int DIR, bool HALF_IN = false, bool HALF_OUT = false>
+__device__ __forceinline__ void dft16(double2* v) {
+  double2 a[4][4];  // a[n2][k1]
+#pragma unroll
+  for (int n2 = 0; n2 < 4; ++n2) {
+    if constexpr (HALF_IN) {
+      const double2 x0 = v[n2], x1 = v[4 + n2], w = mul_w4<DIR>(x1);
+      a[n2][0] = cadd(x0, x1);
+      a[n2][1] = cadd(x0, w);
+      a[n2][2] = csub(x0, x1);
+      a[n2][3] = csub(x0, w);
+    } else {
+      a[n2][0] = v[n2];
+      a[n2][1] = v[4 + n2];
+      a[n2][2] = v[8 + n2];
+      a[n2][3] = v[12 + n2];
+      dft4<DIR>(a[n2][0], a[n2][1], a[n2][2], a[n2][3]);
+    }
+  }
+  a[1][1] = mul_w16<DIR>(a[1][1]);
+  a[1][2] = mul_w8<DIR>(a[1][2]);
+  a[1][3] = mul_w163<DIR>(a[1][3]);
+  a[2][1] = mul_w8<DIR>(a[2][1]);
+  a[2][2] = mul_w4<DIR>(a[2][2]);
+  a[2][3] = mul_w83<DIR>(a[2][3]);
+  a[3][1] = mul_w163<DIR>(a[3][1]);
+  a[3][2] = mul_w83<DIR>(a[3][2]);
+  {
+    const double2 m = mul_w16<DIR>(a[3][3]);  // w16^9 = -w16
+    a[3][3] = make_double2(-m.x, -m.y);
+  }
+#pragma unroll
+  for (int k1 = 0; k1 < 4; ++k1) {
+    const double2 e0 = cadd(a[0][k1], a[2][k1]), e1 = csub(a[0][k1], a[2][k1]);
+    const double2 o0 = cadd(a[1][k1], a[3][k1]), o1 = mul_w4<DIR>(csub(a[1][k1], a[3][k1]));
+    v[k1] = cadd(e0, o0);
+    v[k1 + 4] = cadd(e1, o1);
+    if constexpr (!HALF_OUT) {
+      v[k1 + 8] = csub(e0, o0);
+      v[k1 + 12] = csub(e1, o1);
+    }
+  }
+}
+
 template <int R, int DIR>
 __device__ __forceinline__ void dftR(double2* v) {
   if constexpr (R == 2) dft2<DIR>(v);
   else if constexpr (R == 4) dft4<DIR>(v);
-  else dft8<DIR>(v);
+  else if constexpr (R == 8) dft8<DIR>(v);
+  else dft16<DIR>(v);
 }
 
 // ------------------------------------------------------------------------ plans

@@ -45,6 +45,7 @@ struct ApplyParams {
   const double2* tw_y;   // L = 2ny, forward order
   const double2* tw_z;   // L = 2nz, forward order
   const double2* tw_zr;  // L = 2nz, reversed order
+  const double2* pw_z;   // exp(-2 pi i m / 2nz), m < 2nz (radix-16 z-pass)
   int n_items;
   ApplyItem items[kMaxItems];
 };
@@ -52,7 +53,9 @@ struct ApplyParams {
 struct Twiddles {
   double2* dev = nullptr;
   int off[kMaxLog2 + 1][2] = {};  // [log2 L][order]
+  int pw[kMaxLog2 + 1] = {};      // [log2 L]: exp(-2 pi i m / L), m = 0 .. L-1
   const double2* get(int L, int rev) const;
+  const double2* powers(int L) const;
 };
 
 struct GreenSpec {

@@ -14,12 +14,19 @@
 #include <unordered_map>
 #include <vector>
 
+#include "bulk_copy.cuh"
 #include "fft_core.cuh"
 #include "ie_internal.h"
 
 namespace ie {
 
 __device__ __forceinline__ double2 ld2(const double2* p) { return __ldg(p); }
+// read-only load that does not allocate in L1 (streamed data must not evict L1-resident tables)
+__device__ __forceinline__ double2 ld2_stream(const double2* p) {
+  double2 v;
+  asm("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+  return v;
+}
 
 // =====================================================================  K-A
 template <int L>
@@ -205,6 +212,212 @@ __global__ void __launch_bounds__(256) k_zconv(const __grid_constant__ ApplyPara
   }
 }
 
+// =====================================================================  K-C (radix 16)
+// The same z-convolution for L = 2nz in {64, 128, 256} as two Stockham stages, radix 16
+// then R1 = L/16 (inverse: R1 then 16), so each FFT crosses shared memory once.
+//  * the tile (W consecutive kx at one ky, the nz non-zero rows of the 3 components,
+//    W*16 B per row) is staged into shared memory by per-thread asynchronous copies
+//    (LDGSTS), and the packed-Green rows the tile will need are prefetched into L2 at the
+//    same time, so the spectral multiply later finds them on chip;
+//  * T = L/16 threads per column, 16 values each; the first forward butterfly skips the
+//    zero upper half, the last inverse butterfly produces only the kept lower half;
+//  * the three spectra are parked in shared memory; the multiply walks the octant index iz
+//    and serves the mirror pair kz = iz, L - iz from one read of the 6 Green components
+//    (half the loads of a per-kz walk); the first batch of those loads is issued before
+//    the last forward FFT, the second before the first batch is consumed;
+//  * 128 threads and 100 KB per CTA: two CTAs per SM, so one CTA's copies and loads
+//    overlap the other's arithmetic.
+// Shared layout: element (i, c) of a region at R[i*W + c]; an 8-lane phase of a 128-bit
+// access is 8 consecutive c, i.e. 128 contiguous bytes: conflict-free.
+__device__ __forceinline__ double2 flip_if(double2 a, unsigned neg) {  // sign flip without FP64 ops
+  return make_double2(__hiloint2double(__double2hiint(a.x) ^ (int)neg, __double2loint(a.x)),
+                      __hiloint2double(__double2hiint(a.y) ^ (int)neg, __double2loint(a.y)));
+}
+// y = g0 j0 + g1 j1 + g2 j2 as fused chains (6 FP64 ops per real/imag part)
+__device__ __forceinline__ double2 cdot3(double2 g0, double2 j0, double2 g1, double2 j1, double2 g2, double2 j2) {
+  double re = -g2.y * j2.y;
+  re = fma(g2.x, j2.x, re);
+  re = fma(-g1.y, j1.y, re);
+  re = fma(g1.x, j1.x, re);
+  re = fma(-g0.y, j0.y, re);
+  re = fma(g0.x, j0.x, re);
+  double im = g2.y * j2.x;
+  im = fma(g2.x, j2.y, im);
+  im = fma(g1.y, j1.x, im);
+  im = fma(g1.x, j1.y, im);
+  im = fma(g0.y, j0.x, im);
+  im = fma(g0.x, j0.y, im);
+  return make_double2(re, im);
+}
+
+template <int L, int W>
+__global__ void __launch_bounds__(128, 2) k_zconv16(const __grid_constant__ ApplyParams p) {
+  constexpr int T = L / 16, R1 = L / 16, U = 16 / R1, NZ = L / 2;
+  static_assert(L == 64 || L == 128 || L == 256, "radix-16 z-pass: L in {64,128,256}");
+  extern __shared__ __align__(16) double2 sm[];
+  double2* twl = sm + 3 * L * W;  // exp(-2 pi i m / L), m < L
+  const int c = threadIdx.x % W, t = threadIdx.x / W;
+  const ApplyItem& it = p.items[blockIdx.z];
+  const int nx = p.nx, ny = p.ny, Lx = 2 * nx, Ly = 2 * ny;
+  const int kx0 = blockIdx.x * W, kx = kx0 + c;
+  const int by = blockIdx.y;  // mirror pairs (ky, 2ny-ky) adjacent in launch order (L2 reuse of G)
+  const int ky = (by == 0) ? 0 : (by == 1 ? ny : ((by & 1) ? Ly - (by >> 1) : (by >> 1)));
+  const long long cs = (long long)NZ * Ly * Lx, zs = (long long)Ly * Lx;
+  double2* tile = p.X2 + (long long)blockIdx.z * 3 * cs + (long long)ky * Lx + kx0;
+  const long long gcs = (long long)(NZ + 1) * (ny + 1) * (nx + 1);
+  const long long gzs = (long long)(ny + 1) * (nx + 1);
+  const int ix = kx <= nx ? kx : Lx - kx;
+  const int iy = ky <= ny ? ky : Ly - ky;
+  const double2* g = p.ghat + (long long)iy * (nx + 1) + ix;
+
+  // ---- stage the non-zero rows z in [sz0, sz1) (zero the rest) and the twiddle powers;
+  //      prefetch the Green rows (6 components x (nz+1) octant planes) into L2
+  {
+    const int z0 = it.sz0, z1 = it.sz1;
+#pragma unroll
+    for (int l = 0; l < 3; ++l)
+      for (int z = t; z < NZ; z += T) {
+        double2* d = &sm[(l * L + z) * W + c];
+        if (z >= z0 && z < z1) cp_async16(d, tile + l * cs + z * zs + c);
+        else *d = czero();
+      }
+    for (int m = threadIdx.x; m < L; m += blockDim.x) cp_async16(&twl[m], &p.pw_z[m]);
+    const int ixmin = (kx0 + W - 1 <= nx) ? kx0 : Lx - kx0 - (W - 1);  // the tile's ix span (W | nx)
+    const double2* g0 = p.ghat + (long long)iy * (nx + 1) + ixmin;
+    for (int q = threadIdx.x; q < 6 * (NZ + 1); q += blockDim.x) {
+      const double2* row = g0 + (q / (NZ + 1)) * gcs + (q % (NZ + 1)) * gzs;
+      prefetch_l2(row);
+      prefetch_l2(row + (W - 1));
+    }
+    cp_async_wait_all();
+    __syncthreads();
+  }
+
+  // L = 256 (U = 1): forward stage-1 twiddles w^(r t) and inverse ones conj(w^(r t)) are the
+  // same 15 values for every component -- keep them in registers
+  double2 twr[L == 256 ? 16 : 1];
+  if constexpr (L == 256) {
+#pragma unroll
+    for (int r = 1; r < 16; ++r) twr[r] = twl[r * t];
+  }
+  auto tw = [&](int r, int j) -> double2 {
+    if constexpr (L == 256) return twr[r];
+    else return twl[r * j];
+  };
+
+  // ---- forward z-FFT of component l in place; its spectrum (kz = j + 16 r) is parked in
+  //      the thread's own slots
+  auto forward = [&](int l) {
+    double2* S = sm + l * L * W;
+    double2 v[16];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) v[r] = S[(t + r * T) * W + c];  // z = t + r L/16 < nz
+    dft16<-1, true>(v);
+    __syncthreads();  // all inputs of this component read before the exchange overwrites them
+#pragma unroll
+    for (int r = 0; r < 16; ++r) S[(t * 16 + r) * W + c] = v[r];
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int j = t + u * T;
+#pragma unroll
+      for (int r = 0; r < R1; ++r) {
+        double2 x = S[(j + r * 16) * W + c];
+        if (r > 0) x = cmul(x, tw(r, j));
+        v[u * R1 + r] = x;
+      }
+      dftR<R1, -1>(&v[u * R1]);
+#pragma unroll
+      for (int r = 0; r < R1; ++r) S[(j + r * 16) * W + c] = v[u * R1 + r];
+    }
+  };
+
+  // ---- 3x3 spectral multiply: octant plane iz = t + q T serves kz = iz and kz = L - iz; the
+  //      full spectrum is D G_oct D with D = diag(sx, sy, sz) the per-axis mirror signs
+  constexpr int NQ = NZ / T;           // octant planes per thread (plus iz = nz on t = 0)
+  constexpr int B = NQ >= 4 ? NQ / 2 : NQ;  // planes per batch of loads
+  const unsigned fx = kx > nx ? 0x80000000u : 0u, fy = ky > ny ? 0x80000000u : 0u;
+  double2* S0 = sm;
+  double2* S1 = sm + L * W;
+  double2* S2 = sm + 2 * L * W;
+  auto load_batch = [&](double2(&G)[B][6], int q0) {
+#pragma unroll
+    for (int b = 0; b < B; ++b)
+#pragma unroll
+      for (int k = 0; k < 6; ++k) G[b][k] = ld2(g + (t + (q0 + b) * T) * gzs + k * gcs);
+  };
+  auto mult = [&](int kz, unsigned fz, const double2(&G)[6]) {
+    const double2 gxy = flip_if(G[3], fx ^ fy), gxz = flip_if(G[4], fx ^ fz), gyz = flip_if(G[5], fy ^ fz);
+    const int a = kz * W + c;
+    const double2 j0 = S0[a], j1 = S1[a], j2 = S2[a];
+    S0[a] = cdot3(G[0], j0, gxy, j1, gxz, j2);
+    S1[a] = cdot3(gxy, j0, G[1], j1, gyz, j2);
+    S2[a] = cdot3(gxz, j0, gyz, j1, G[2], j2);
+  };
+  auto mult_batch = [&](const double2(&G)[B][6], int q0) {
+#pragma unroll
+    for (int b = 0; b < B; ++b) {
+      const int iz = t + (q0 + b) * T;
+      mult(iz, 0u, G[b]);
+      if (iz != 0) mult(L - iz, 0x80000000u, G[b]);
+    }
+  };
+
+  forward(0);
+  forward(1);
+  double2 Ga[B][6];
+  load_batch(Ga, 0);  // in flight during the last forward FFT
+  forward(2);
+  __syncthreads();
+  if constexpr (2 * B == NQ) {
+    double2 Gb[B][6];
+    load_batch(Gb, B);
+    mult_batch(Ga, 0);
+    mult_batch(Gb, B);
+  } else {
+    mult_batch(Ga, 0);
+  }
+  if (t == 0) {  // iz = nz: kz = nz only (its own mirror)
+    double2 G[6];
+#pragma unroll
+    for (int k = 0; k < 6; ++k) G[k] = ld2(g + NZ * gzs + k * gcs);
+    mult(NZ, 0u, G);
+  }
+  __syncthreads();
+
+  // ---- inverse z-FFTs (radix R1 then 16), crop to z < nz, store
+#pragma unroll 1
+  for (int l = 0; l < 3; ++l) {
+    double2* S = sm + l * L * W;
+    double2 v[16];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int j = t + u * T;
+#pragma unroll
+      for (int r = 0; r < R1; ++r) v[u * R1 + r] = S[(j + r * 16) * W + c];
+      dftR<R1, +1>(&v[u * R1]);
+    }
+    __syncthreads();  // every thread has read its spectrum slots before the exchange
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int j = t + u * T;
+#pragma unroll
+      for (int r = 0; r < R1; ++r) S[(j * R1 + r) * W + c] = v[u * R1 + r];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+      double2 x = S[(t + r * T) * W + c];
+      if (r > 0) x = cmulc(x, tw(r, t));  // exp(+2 pi i r t / L)
+      v[r] = x;
+    }
+    dft16<+1, false, true>(v);
+    double2* dst = tile + l * cs + c;
+#pragma unroll
+    for (int r = 0; r < 8; ++r) dst[(long long)(t + r * T) * zs] = v[r];  // z = t + r L/16 < nz
+  }
+}
+
 // =====================================================================  K-D
 template <int L>
 __global__ void __launch_bounds__(512) k_yinv(const __grid_constant__ ApplyParams p) {
@@ -300,6 +513,7 @@ static void fill_tw(std::vector<double2>& out, bool rev) {
 }
 
 const double2* Twiddles::get(int L, int rev) const { return dev + off[ilog2i(L)][rev ? 1 : 0]; }
+const double2* Twiddles::powers(int L) const { return dev + pw[ilog2i(L)]; }
 
 ie_status build_twiddles(ie_ctx* c) {
   std::vector<double2> h;
@@ -321,6 +535,14 @@ ie_status build_twiddles(ie_ctx* c) {
   add(8, fill_tw<256>);
   add(9, fill_tw<512>);
   add(10, fill_tw<1024>);
+  for (int p = 1; p <= kMaxLog2; ++p) {  // power tables exp(-2 pi i m / L), m < L
+    const long long L = 1LL << p;
+    c->tw.pw[p] = (int)h.size();
+    for (long long m = 0; m < L; ++m) {
+      const long double ang = -2.0L * 3.14159265358979323846264338327950288L * (long double)m / (long double)L;
+      h.push_back(make_double2((double)cosl(ang), (double)sinl(ang)));
+    }
+  }
   IE_CUDA(c, cudaMalloc(&c->tw.dev, h.size() * sizeof(double2)));
   IE_CUDA(c, cudaMemcpy(c->tw.dev, h.data(), h.size() * sizeof(double2), cudaMemcpyHostToDevice));
   return IE_OK;
@@ -411,6 +633,30 @@ static cudaError_t go_zconv(const ApplyParams& p, cudaStream_t s) {
   k_zconv<L><<<dim3(2 * p.nx / W, 2 * p.ny, p.n_items), W * T, smem, s>>>(p);
   return cudaGetLastError();
 }
+// radix-16 z-pass: W columns per CTA with W*T <= 128 and W >= 8 (128-byte rows); returns 0
+// when the shape needs the generic kernel
+static int zconv16_width(int L, int Lx) {
+  if (L != 64 && L != 128 && L != 256) return 0;
+  int W = 128 / (L / 16);
+  while (W > 8 && W > Lx) W /= 2;
+  return (W >= 8 && Lx % W == 0) ? W : 0;
+}
+template <int L, int W>
+static cudaError_t go_zconv16_w(const ApplyParams& p, cudaStream_t s) {
+  const size_t smem = (size_t)(3 * L * W + L) * sizeof(double2);
+  cudaError_t e = prep((const void*)k_zconv16<L, W>, smem);
+  if (e) return e;
+  k_zconv16<L, W><<<dim3(2 * p.nx / W, 2 * p.ny, p.n_items), W * (L / 16), smem, s>>>(p);
+  return cudaGetLastError();
+}
+static cudaError_t go_zconv16(const ApplyParams& p, cudaStream_t s, int W) {
+  const int L = 2 * p.nz;
+  if (L == 256) return go_zconv16_w<256, 8>(p, s);
+  if (L == 128) return W == 16 ? go_zconv16_w<128, 16>(p, s) : go_zconv16_w<128, 8>(p, s);
+  if (L == 64)
+    return W == 32 ? go_zconv16_w<64, 32>(p, s) : (W == 16 ? go_zconv16_w<64, 16>(p, s) : go_zconv16_w<64, 8>(p, s));
+  return cudaErrorInvalidValue;
+}
 template <int L>
 static cudaError_t go_yinv(const ApplyParams& p, cudaStream_t s) {
   const int T = FftPlan<L>::T, W = y_width(T, 2 * p.nx);
@@ -456,7 +702,11 @@ static cudaError_t run_apply(const ApplyParams& p, cudaStream_t s, cudaEvent_t* 
   IE_DISPATCH_L(2 * p.ny, wrap_yfwd, &e, p, s, max_planes);
   if (e) return e;
   mark(2);
-  IE_DISPATCH_L(2 * p.nz, wrap_zconv, &e, p, s);
+  if (const int W16 = zconv16_width(2 * p.nz, 2 * p.nx)) {
+    e = go_zconv16(p, s, W16);
+  } else {
+    IE_DISPATCH_L(2 * p.nz, wrap_zconv, &e, p, s);
+  }
   if (e) return e;
   mark(3);
   IE_DISPATCH_L(2 * p.ny, wrap_yinv, &e, p, s);
@@ -478,6 +728,7 @@ ie_status launch_apply(ie_ctx* c, ApplyParams& p) {
   p.tw_y = c->tw.get(2 * p.ny, 0);
   p.tw_z = c->tw.get(2 * p.nz, 0);
   p.tw_zr = c->tw.get(2 * p.nz, 1);
+  p.pw_z = c->tw.powers(2 * p.nz);
   cudaEvent_t* ev = nullptr;
   if (c->profiling) {
     while (c->ev_pool.size() < c->ev_used + 6) {
