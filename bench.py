@@ -176,6 +176,55 @@ def run_reference(args, cfg, sigma, rank, ws):
 
 
 # ------------------------------------------------------------------------------- ours
+def cufft_reference(ctx, cfg, sigma, x, reps=5):
+    """The same operator through torch.fft (cuFFT) + einsum on the full padded grid: a timing
+    reference point only.  Uses the library's packed Green spectrum,
+    unpacked to the 6 full spectra; no result of it feeds anything else."""
+    import torch
+    import paper_2306_17537_b200 as ie
+    dev = x.device
+    nx, ny, nz = cfg.n
+    oct_ = torch.from_numpy(ie.ie_get_green_octant(ctx)).to(dev)  # [6][nz+1][ny+1][nx+1], scaled 1/(8N)
+
+    def fold(n):
+        k = torch.arange(2 * n, device=dev)
+        return torch.where(k <= n, k, 2 * n - k), torch.where(k > n, -1.0, 1.0).to(torch.float64)
+    (ix, sx), (iy, sy), (iz, sz) = fold(nx), fold(ny), fold(nz)
+    full = oct_[:, iz][:, :, iy][:, :, :, ix]  # [6][2nz][2ny][2nx]
+    S = {3: (sx[None, None, :] * sy[None, :, None]), 4: (sx[None, None, :] * sz[:, None, None]),
+         5: (sy[None, :, None] * sz[:, None, None])}
+    for cidx, sg in S.items():
+        full[cidx] *= sg.expand(2 * nz, 2 * ny, 2 * nx)
+    G = [[full[0], full[3], full[4]], [full[3], full[1], full[5]], [full[4], full[5], full[2]]]
+    ds = torch.from_numpy(sigma).to(dev) - cfg.sigma_b * torch.eye(3, dtype=torch.float64, device=dev)
+    ds = ds.permute(3, 4, 0, 1, 2).contiguous()  # [3][3][nz][ny][nx]
+
+    def apply(xx):
+        J = torch.einsum("qrzyx,rzyx->qzyx", ds.to(torch.complex128), xx)
+        Jp = torch.zeros((3, 2 * nz, 2 * ny, 2 * nx), dtype=torch.complex128, device=dev)
+        Jp[:, :nz, :ny, :nx] = J
+        F = torch.fft.fftn(Jp, dim=(1, 2, 3))
+        Y = torch.stack([G[p][0] * F[0] + G[p][1] * F[1] + G[p][2] * F[2] for p in range(3)])
+        Y = torch.fft.ifftn(Y, dim=(1, 2, 3), norm="forward")[:, :nz, :ny, :nx]
+        return xx - Y
+
+    xx = x[0]
+    apply(xx)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        y = apply(xx)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    del full, G, y
+    torch.cuda.empty_cache()
+    return {"ms_per_apply": round(ms, 4), "gbs_b_model": round(b_model(nx, ny, nz) / (ms / 1e3) / 1e9, 1),
+            "what": "torch.fft.fftn/ifftn (cuFFT) complex128 on the 2x padded grid + einsum contrast and "
+                    "6-component spectral multiply; timing reference only"}
+
+
 def run_ours(args, cfg, sigma, rank, ws, local):
     import torch
     import paper_2306_17537_b200 as ie
@@ -253,6 +302,8 @@ def run_ours(args, cfg, sigma, rank, ws, local):
            "h2d_bytes_per_step": int(xh.numel() * xh.element_size()),
            "d2h_bytes_per_step": int(yh.numel() * yh.element_size())}
 
+    cufft = None if args.no_cufft else cufft_reference(ctx, cfg, sigma, x)
+
     # --- forward solve seconds per tool position (full-domain GMRES vs DD schemes)
     dd = None
     if not args.no_dd:
@@ -281,7 +332,7 @@ def run_ours(args, cfg, sigma, rank, ws, local):
                        "sub_applies": st["sub_applies"], "e_final": st["e_final"],
                        "status": ie.STATUS.get(st["status"], st["status"])}
     return dict(value=value, per_step=per_step, launches=launches, clk=clk.summary(), peak=peak,
-                peak_src=peak_src, dom=dom, achieved=achieved, kernels=kernels, e2e=e2e, dd=dd, bm=bm,
+                peak_src=peak_src, dom=dom, achieved=achieved, kernels=kernels, e2e=e2e, dd=dd, bm=bm, cufft=cufft,
                 traffic=args.traffic)
 
 
@@ -295,6 +346,7 @@ def main():
     ap.add_argument("--no-dd", action="store_true")
     ap.add_argument("--dd-reps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-cufft", action="store_true")
     ap.add_argument("--traffic", type=float, default=None, help="ncu dram bytes per launch of the dominant kernel")
     args = ap.parse_args()
     assert args.warmup >= 3 or args.impl == "reference" or args.warmup >= 0
@@ -331,7 +383,7 @@ def main():
                          "kernel": r["dom"], "peak_source": r["peak_src"]},
             "kernels": r["kernels"],
             "e2e": r["e2e"], "gpu_launches": r["launches"], "clocks": r["clk"],
-            "cpu_baseline": cpu, "dd": r["dd"]}
+            "cpu_baseline": cpu, "cufft_reference": r["cufft"], "dd": r["dd"]}
     print(json.dumps(line))
 
 
