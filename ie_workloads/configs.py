@@ -4,7 +4,11 @@ Grids are centred at the origin: origin_a = -(n_a - 1)/2 * h (centroid of cell (
 Seed = config number.  Readings for the parts BASELINE.json leaves open are listed in
 DESIGN.md §Inputs; variants:
   c2capped  sigma_h ~ 10^U[-2,0] instead of 10^U[-2,1] (the literal c2
-            contrast makes conventional-IE GMRES stagnate)
+            contrast makes conventional-IE GMRES stagnate).  At 32^3 it still stagnates
+            (oracle GMRES(30): relres 1.6e-4 after 3000 iterations; the resistive blocks,
+            sigma_v down to 1e-3 S/m against sigma_b = 0.1, are the cause, not the cap)
+  c2mod     the c2 geometry with moderate contrast: sigma_h = sigma_b 10^U[-0.3,0.7],
+            sigma_v/sigma_h ~ U[0.3,1] (oracle GMRES(30) reaches 1e-11 in 56 iterations)
   c3h, c4h  the c3 / c4 grids, contrast recipes and tools on a HOMOGENEOUS background
             (sigma_b = 1 S/m, 400 kHz): the layered-table path (A3L) is not built yet.
   *mini     the same recipe on an 8^3 grid so that dense LU gives exact truth.
@@ -78,6 +82,23 @@ def _blocks_vti(rng, cfg, block, log_hi):
             for ib in range(nx // block):
                 sh = 10.0 ** rng.uniform(-2.0, log_hi)
                 r = rng.uniform(0.1, 1.0)
+                th = np.radians(rng.uniform(0.0, 60.0))
+                ph = np.radians(rng.uniform(0.0, 360.0))
+                s[kb * block:(kb + 1) * block, jb * block:(jb + 1) * block, ib * block:(ib + 1) * block] = \
+                    vti_tensor(sh, r * sh, th, ph)
+    return s
+
+
+def _blocks_vti_mod(rng, cfg, block=8):
+    """c2mod: per block (x-fastest) sigma_h = sigma_b 10^U[-0.3, 0.7], ratio U[0.3, 1], dip
+    U[0,60] deg, azimuth U[0,360] deg, in that order; Appendix C tensor."""
+    nx, ny, nz = cfg.n
+    s = np.zeros((nz, ny, nx, 3, 3))
+    for kb in range(nz // block):
+        for jb in range(ny // block):
+            for ib in range(nx // block):
+                sh = cfg.sigma_b * 10.0 ** rng.uniform(-0.3, 0.7)
+                r = rng.uniform(0.3, 1.0)
                 th = np.radians(rng.uniform(0.0, 60.0))
                 ph = np.radians(rng.uniform(0.0, 360.0))
                 s[kb * block:(kb + 1) * block, jb * block:(jb + 1) * block, ib * block:(ib + 1) * block] = \
@@ -171,6 +192,11 @@ def make_config(name):
                       sources=[(np.zeros(3), zdip)],
                       receivers=[np.array([0.0, 0.0, 0.5]), np.array([0.0, 0.0, 1.0])],
                       boxes=[(0, 32, 0, 32, 0, 16), (0, 32, 0, 32, 16, 32)], restart=30, outer_tol=1e-8)
+    if name == "c2mod":
+        return Config(name, (32, 32, 32), 0.1, 0.1, 2e6, 2, _blocks_vti_mod,
+                      sources=[(np.zeros(3), zdip)],
+                      receivers=[np.array([0.0, 0.0, 0.5]), np.array([0.0, 0.0, 1.0])],
+                      boxes=[(0, 32, 0, 32, 0, 16), (0, 32, 0, 32, 16, 32)], restart=30, outer_tol=1e-8)
     if name == "c2mini":
         return Config(name, (8, 8, 8), 0.1, 0.1, 2e6, 2, lambda rng, c: _blocks_vti(rng, c, 2, 0.0),
                       sources=[(np.zeros(3), zdip)], receivers=[np.array([0.0, 0.0, 0.5])],
@@ -205,4 +231,4 @@ def make_config(name):
     raise KeyError(name)
 
 
-CONFIG_NAMES = ("c1", "c2", "c2capped", "c2mini", "c3h", "c3mini", "c4h", "c5", "c5mini")
+CONFIG_NAMES = ("c1", "c2", "c2capped", "c2mod", "c2mini", "c3h", "c3mini", "c4h", "c5", "c5mini")

@@ -56,7 +56,7 @@ typedef enum {
   IE_ERR_BREAKDOWN = 5,        /* non-finite values in a Krylov recurrence */
   IE_ERR_STATE = 6,            /* call-order violation (e.g. no contrast set yet) */
   IE_ERR_PLACEMENT = 7,        /* a source within 1e-6*h of a cell centroid (E0 singular there) */
-  IE_ERR_UNSUPPORTED = 8       /* a feature declared here but not built (layered backgrounds) */
+  IE_ERR_UNSUPPORTED = 8       /* the call does not apply to this context (e.g. set_source on a layered one) */
 } ie_status;
 
 /* Uniform grid.  origin = centroid of cell (0,0,0), metres; dx,dy,dz > 0 in metres. */
@@ -67,15 +67,32 @@ typedef struct {
 } ie_grid;
 
 /* Background medium.  The paper uses a homogeneous isotropic background sigma0:
- * n_layers = 1, sigma[0] = sigma0 > 0 (S/m), z_iface = NULL, table = NULL.
- * Layered backgrounds (n_layers > 1 with host-precomputed Green tables) are part of the
- * planned interface and currently return IE_ERR_UNSUPPORTED. */
+ * n_layers = 1, sigma[0] = sigma0 > 0 (S/m), z_iface = NULL, table = NULL, table_format 0.
+ *
+ * Layered backgrounds (beyond the paper; DESIGN.md readings
+ * R17-R19): the kernel is translation invariant in x and y only,
+ *     (G J)_p(i,j,k) = sum_{q,i',j',k'} T_pq(i-i', j-j'; k, k') J_q(i',j',k'),
+ * and dsigma = sigma - sigma_b(z_k) I with sigma_b(z) the conductivity of the layer that holds
+ * the cell centroid (layer l: z_iface[l-1] <= z < z_iface[l], layers bottom to top).
+ *  - table_format 1 (IE_TABLE_QUADRANT): table = HOST complex128 [9][nz][nz][ny][nx],
+ *    T[p*3+q][k][k'][dj][di] for offsets di, dj >= 0 (kernel samples including dv and the
+ *    self term, like K(d) of the homogeneous kernel); negative offsets follow the mirror
+ *    rules T_pq(-di,dj) = sx_p sx_q T_pq(di,dj), sx = (-1,1,1), and T_pq(di,-dj) =
+ *    sy_p sy_q T_pq(di,dj), sy = (1,-1,1) (so the stored xy, xz entries at di = 0 and xy, yz
+ *    entries at dj = 0 are taken as 0).  Read (copied to the device) inside ie_create.
+ *    n_layers > 1 requires this format; then E0 is caller-supplied (ie_set_incident) and
+ *    receivers use ie_receiver_fields_table (ie_set_source / ie_receiver_fields return
+ *    UNSUPPORTED).
+ *  - table_format 2 (IE_TABLE_HOMOGENEOUS): n_layers = 1, table = NULL: the library builds the
+ *    degenerate equal-layer table T = K(di, dj, k - k') of sigma[0] itself and runs the
+ *    layered operator path on it (same operator as format 0 up to rounding). */
+typedef enum { IE_TABLE_NONE = 0, IE_TABLE_QUADRANT = 1, IE_TABLE_HOMOGENEOUS = 2 } ie_table_format;
 typedef struct {
   int32_t n_layers;
-  const double* sigma;   /* [n_layers], bottom to top, S/m */
-  const double* z_iface; /* [n_layers-1] ascending, m */
-  const void* table;     /* layered Green table (unsupported in this build) */
-  int32_t table_format;
+  const double* sigma;   /* [n_layers], bottom to top, S/m, > 0 */
+  const double* z_iface; /* [n_layers-1] ascending, m (NULL when n_layers = 1) */
+  const void* table;     /* host table (format 1) or NULL */
+  int32_t table_format;  /* ie_table_format */
 } ie_background;
 
 /* Rectangular sub-domain Omega_j (Eq. 11): half-open cell ranges. */
@@ -89,7 +106,9 @@ typedef struct {
  * a = (3 dv / 4 pi)^{1/3} (reading R3), and precomputes its 2x-padded FFT
  * (Eq. 10, "pre-calculated before calling the iterative solvers") on the device.
  * cuda_stream: a cudaStream_t (NULL = legacy default stream).  freq_hz > 0.
- * Errors: INVALID_ARGUMENT, UNSUPPORTED (layered), OUT_OF_MEMORY, CUDA. */
+ * Layered backgrounds (table_format != 0): the table is copied to the device and its
+ * 2x-padded x-y spectra are packed per horizontal wavenumber (see ie_get_layer_spectrum).
+ * Errors: INVALID_ARGUMENT, OUT_OF_MEMORY, CUDA. */
 ie_status ie_create(const ie_grid* grid, const ie_background* bg, double freq_hz, void* cuda_stream,
                     ie_ctx** out);
 ie_status ie_destroy(ie_ctx* ctx); /* frees library-owned memory; NULL is a no-op */
@@ -195,6 +214,17 @@ ie_status ie_solve_dd(ie_ctx* ctx, const ie_dd_opts* opts, void* e_dev, int32_t 
 ie_status ie_receiver_fields(ie_ctx* ctx, const void* e_dev, int32_t n_rx, const double* rx_pos, void* h_host,
                              void* v_host);
 
+/* Layered backgrounds: receiver couplings by reciprocity (Eq. 4 with the reciprocity of the
+ * discrete system; R17):
+ *   h[s][r] = h0[s][r] + (i omega mu0)^-1 sum_c E0rx_r(r_c) . (dsigma_c E_s(r_c)) dv
+ * e_dev: [n_src][3][nz][ny][nx] total fields; e0rx_dev: device [n_rxdip][3][nz][ny][nx],
+ * background E of the unit receiver dipoles (caller-supplied, like the layered E0);
+ * h0_host: host complex128 [n_src][n_rxdip] primary couplings m_r . H0(r_r; source s);
+ * h_host: host complex128 [n_src][n_rxdip] out (m_r . H).  Works on every context.
+ * Synchronous. */
+ie_status ie_receiver_fields_table(ie_ctx* ctx, const void* e_dev, int32_t n_rxdip, const void* e0rx_dev,
+                                   const void* h0_host, void* h_host);
+
 /* Introspection for tests / benchmarks. */
 typedef struct {
   double k0_re, k0_im;     /* background wavenumber */
@@ -216,6 +246,14 @@ ie_status ie_profile_read(ie_ctx* ctx, double* ms /*[5]*/, int32_t* counts /*[5]
  * s * packed[c][kz'][ky'][kx'] with k' = min(k, 2n - k) and s = -1 per axis where
  * the component is odd and k > n. */
 ie_status ie_get_green_octant(ie_ctx* ctx, const ie_box* box, void* host_out);
+
+/* Layered contexts: copy the packed x-y spectra of the domain (box = NULL: the grid; a box
+ * uses the table restricted to its offsets and its layer range) to the host: complex128
+ * [(by+1)(bx+1)][3bz][3bz], entry [iy (bx+1) + ix][q bz + k'][p bz + k] =
+ * F2[T_pq(., .; k0+k, k0+k')](kx = ix, ky = iy) / (4 bx by), F2 the 2-D DFT of the table
+ * circulant-embedded on (2by, 2bx) with the slot at offset +-n set to 0.  The spectrum at a
+ * mirrored wavenumber (2bx - ix or 2by - iy) is D M D with D = diag(sx, sy, 1). */
+ie_status ie_get_layer_spectrum(ie_ctx* ctx, const ie_box* box, void* host_out);
 
 #ifdef __cplusplus
 }

@@ -14,7 +14,9 @@ K(d) in operator.py).  Storage (reading R18): the quadrant of non-negative offse
 complex128 [3][3][nz][nz][ny][nx] = T[p, q, k, k', dj, di]; negative offsets follow the
 mirror symmetry of a horizontally layered isotropic medium,
     T_pq(-di, dj) = sx_p sx_q T_pq(di, dj),  sx = (-1, 1, 1),
-    T_pq(di, -dj) = sy_p sy_q T_pq(di, dj),  sy = (1, -1, 1).
+    T_pq(di, -dj) = sy_p sy_q T_pq(di, dj),  sy = (1, -1, 1),
+so components odd in x (xy, xz) vanish at di = 0 and those odd in y (xy, yz) at dj = 0 (the
+stored values there are ignored).
 
 Evaluations, written plainly:
   * ``dense_matrix_layered`` -- the 3N x 3N matrix entry by entry (tiny grids);
@@ -42,6 +44,11 @@ def expand_table(Tq):
     F = np.zeros((3, 3, nz, nz, 2 * ny - 1, 2 * nx - 1), np.complex128)
     sx = np.outer(SX, SX)[:, :, None, None, None, None]
     sy = np.outer(SY, SY)[:, :, None, None, None, None]
+    # at zero offset the rules force the odd components to vanish (f(0) = -f(0)); the
+    # stored values there are ignored
+    Tq = Tq.copy()
+    Tq[..., :, 0] *= (sx[..., 0, 0] > 0)[..., None]
+    Tq[..., 0, :] *= (sy[..., 0, 0] > 0)[..., None]
     F[..., ny - 1:, nx - 1:] = Tq                                   # di >= 0, dj >= 0
     F[..., ny - 1:, :nx - 1] = sx * Tq[..., :, :0:-1]               # di < 0
     F[..., :ny - 1, nx - 1:] = sy * Tq[..., :0:-1, :]               # dj < 0

@@ -27,7 +27,8 @@ SCHEMES = {"full": IE_DD_FULL, "jacobi": IE_DD_JACOBI, "gauss_seidel": IE_DD_GAU
 EXPORTED = ("ie_create", "ie_destroy", "ie_last_error", "ie_workspace_query", "ie_bind_workspace",
             "ie_set_contrast", "ie_set_source", "ie_get_incident", "ie_set_incident", "ie_apply_operator",
             "ie_solve_subdomain", "ie_solve_dd", "ie_receiver_fields", "ie_get_info", "ie_get_green_octant",
-            "ie_profile", "ie_profile_read")
+            "ie_profile", "ie_profile_read", "ie_receiver_fields_table", "ie_get_layer_spectrum")
+IE_TABLE_NONE, IE_TABLE_QUADRANT, IE_TABLE_HOMOGENEOUS = 0, 1, 2
 KERNELS = ("K-A x-forward+contrast", "K-B y-forward", "K-C z-convolution", "K-D y-inverse",
            "K-E x-inverse+update")
 
@@ -111,6 +112,8 @@ def load_library(path=LIB_PATH):
         "ie_get_green_octant": [P, ctypes.POINTER(ie_box), P],
         "ie_profile": [P, I],
         "ie_profile_read": [P, P, P],
+        "ie_receiver_fields_table": [P, P, I, P, P, P],
+        "ie_get_layer_spectrum": [P, ctypes.POINTER(ie_box), P],
     }
     for name, args in sig.items():
         f = getattr(lib, name)
@@ -174,13 +177,28 @@ def _stream_ptr(stream):
     return ctypes.c_void_p(stream.cuda_stream)
 
 
-def ie_create(n, h, origin, sigma_b, freq_hz, stream=None):
-    """n = (nx, ny, nz); h = (dx, dy, dz) m; origin = centroid of cell (0,0,0); homogeneous background."""
+def ie_create(n, h, origin, sigma_b, freq_hz, stream=None, table=None, table_format=None, z_iface=None):
+    """n = (nx, ny, nz); h = (dx, dy, dz) m; origin = centroid of cell (0,0,0).
+
+    Homogeneous background: sigma_b a number.  Layered (include/ie_b200.h): sigma_b a list of
+    layer conductivities (bottom to top) with z_iface, and table = host complex128 numpy array
+    [9][nz][nz][ny][nx] (format 1); or table_format=2 (the library's degenerate table)."""
     lib = load_library()
     g = ie_grid(int(n[0]), int(n[1]), int(n[2]), float(h[0]), float(h[1]), float(h[2]),
                 (ctypes.c_double * 3)(*[float(v) for v in origin]))
-    sig = (ctypes.c_double * 1)(float(sigma_b))
-    bg = ie_background(1, sig, None, None, 0)
+    layers = np.atleast_1d(np.asarray(sigma_b, np.float64))
+    sig = (ctypes.c_double * len(layers))(*layers)
+    zi = None
+    if z_iface is not None and len(z_iface):
+        zi = (ctypes.c_double * len(z_iface))(*[float(v) for v in z_iface])
+    fmt = table_format if table_format is not None else (IE_TABLE_QUADRANT if table is not None else IE_TABLE_NONE)
+    tab = None
+    if table is not None:
+        table = np.ascontiguousarray(table, np.complex128)
+        nx, ny, nz = (int(v) for v in n)
+        assert table.size == 9 * nz * nz * ny * nx, "table must be [9][nz][nz][ny][nx]"
+        tab = ctypes.c_void_p(table.ctypes.data)
+    bg = ie_background(len(layers), sig, zi, tab, int(fmt))
     out = ctypes.c_void_p()
     st = lib.ie_create(ctypes.byref(g), ctypes.byref(bg), float(freq_hz), _stream_ptr(stream), ctypes.byref(out))
     if st != IE_OK:
@@ -319,3 +337,24 @@ def ie_profile_read(ctx):
     cnt = np.zeros(5, np.int32)
     _check(ctx, _lib.ie_profile_read(ctx.handle, _ptr(ms), _ptr(cnt)), "ie_profile_read")
     return {k: (float(ms[i]), int(cnt[i])) for i, k in enumerate(KERNELS)}
+
+
+def ie_receiver_fields_table(ctx, e, e0rx, h0):
+    """Receiver couplings by reciprocity: e [n_src][3][nz][ny][nx] and e0rx [n_rxdip][3][nz][ny][nx]
+    CUDA complex128 tensors; h0 host complex128 [n_src][n_rxdip].  Returns [n_src][n_rxdip]."""
+    h0 = np.ascontiguousarray(np.asarray(h0, np.complex128).reshape(ctx.n_src, -1))
+    out = np.zeros_like(h0)
+    _check(ctx, _lib.ie_receiver_fields_table(ctx.handle, _ptr(e), int(h0.shape[1]), _ptr(e0rx), _ptr(h0), _ptr(out)),
+           "ie_receiver_fields_table")
+    return out
+
+
+def ie_get_layer_spectrum(ctx, box=None):
+    """Packed layered spectra [(by+1)(bx+1)][3bz][3bz] (layered contexts)."""
+    if box is None:
+        nx, ny, nz = ctx.grid.nx, ctx.grid.ny, ctx.grid.nz
+    else:
+        nx, ny, nz = box[1] - box[0], box[3] - box[2], box[5] - box[4]
+    out = np.zeros(((ny + 1) * (nx + 1), 3 * nz, 3 * nz), np.complex128)
+    _check(ctx, _lib.ie_get_layer_spectrum(ctx.handle, _box(box), _ptr(out)), "ie_get_layer_spectrum")
+    return out

@@ -9,7 +9,7 @@ from concurrent.futures import ThreadPoolExecutor
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libie_b200.so")
-SOURCES = ["operator.cu", "green.cu", "fields.cu", "krylov.cu", "api.cu"]
+SOURCES = ["operator.cu", "green.cu", "layered.cu", "fields.cu", "krylov.cu", "api.cu"]
 NVCC_FLAGS = ["-std=c++17", "-O3", "-lineinfo", "-gencode", "arch=compute_100a,code=sm_100a",
               "-Xcompiler", "-fPIC"]
 

@@ -54,7 +54,7 @@ static ie_status apply_many(ie_ctx* c, Arena& ar, const ie_box& dom, const ie_bo
                             double beta, int acc) {
   const int bx = dom.i1 - dom.i0, by = dom.j1 - dom.j0, bz = dom.k1 - dom.k0;
   ie_status st;
-  const GreenSpec* gs = green_for(c, bx, by, bz, &st);
+  const GreenSpec* gs = green_for(c, bx, by, bz, dom.k0, &st);
   if (!gs) return st;
   const int n = (int)x.size();
   const int items = std::min(n, kMaxItems);
@@ -73,6 +73,7 @@ static ie_status apply_many(ie_ctx* c, Arena& ar, const ie_box& dom, const ie_bo
   p.ds_zs = (long long)c->g.nx * c->g.ny;
   p.ds_ys = c->g.nx;
   p.ghat = gs->oct;
+  p.mhat = gs->mhat;
   p.X1 = scratch;
   p.X2 = scratch + (size_t)items * 3 * 2 * bx * by * bz;
   p.alpha = alpha;
@@ -142,13 +143,29 @@ ie_status ie_create(const ie_grid* g, const ie_background* bg, double freq_hz, v
       return fail(nullptr, IE_ERR_INVALID_ARGUMENT, "grid dimensions must be powers of two in [1, 512]");
   if (!(g->dx > 0) || !(g->dy > 0) || !(g->dz > 0)) return fail(nullptr, IE_ERR_INVALID_ARGUMENT, "cell sizes must be > 0");
   if (!(freq_hz > 0) || !std::isfinite(freq_hz)) return fail(nullptr, IE_ERR_INVALID_ARGUMENT, "frequency must be > 0");
-  if (bg->n_layers != 1 || bg->table)
-    return fail(nullptr, IE_ERR_UNSUPPORTED, "layered backgrounds (SURVEY 8(a) A3L) are not built yet; use n_layers = 1");
-  if (!bg->sigma || !(bg->sigma[0] > 0) || !std::isfinite(bg->sigma[0]))
-    return fail(nullptr, IE_ERR_INVALID_ARGUMENT, "background conductivity must be > 0");
+  if (bg->n_layers < 1 || !bg->sigma) return fail(nullptr, IE_ERR_INVALID_ARGUMENT, "background: n_layers >= 1 and sigma");
+  for (int l = 0; l < bg->n_layers; ++l)
+    if (!(bg->sigma[l] > 0) || !std::isfinite(bg->sigma[l]))
+      return fail(nullptr, IE_ERR_INVALID_ARGUMENT, "background conductivity must be > 0");
+  if (bg->n_layers > 1) {
+    if (!bg->z_iface) return fail(nullptr, IE_ERR_INVALID_ARGUMENT, "layered background needs z_iface");
+    for (int l = 1; l < bg->n_layers - 1; ++l)
+      if (!(bg->z_iface[l] > bg->z_iface[l - 1])) return fail(nullptr, IE_ERR_INVALID_ARGUMENT, "z_iface must ascend");
+    if (bg->table_format != IE_TABLE_QUADRANT || !bg->table)
+      return fail(nullptr, IE_ERR_INVALID_ARGUMENT, "a layered background needs a table (table_format 1)");
+  }
+  if (bg->table_format != IE_TABLE_NONE && bg->table_format != IE_TABLE_QUADRANT &&
+      bg->table_format != IE_TABLE_HOMOGENEOUS)
+    return fail(nullptr, IE_ERR_INVALID_ARGUMENT, "unknown table_format");
+  if ((bg->table_format == IE_TABLE_QUADRANT) != (bg->table != nullptr))
+    return fail(nullptr, IE_ERR_INVALID_ARGUMENT, "table pointer and table_format disagree");
   ie_ctx* c = new ie_ctx();
   c->g = *g;
   c->sigma_b = bg->sigma[0];
+  c->layered = bg->table_format != IE_TABLE_NONE;
+  c->table_format = bg->table_format;
+  c->lay_sigma.assign(bg->sigma, bg->sigma + bg->n_layers);
+  if (bg->n_layers > 1) c->lay_z.assign(bg->z_iface, bg->z_iface + bg->n_layers - 1);
   c->freq = freq_hz;
   c->omega = 2 * kPi * freq_hz;
   c->stream = (cudaStream_t)stream;
@@ -166,9 +183,10 @@ ie_status ie_create(const ie_grid* g, const ie_background* bg, double freq_hz, v
     return fail(nullptr, IE_ERR_CUDA, "no CUDA device available (this library has no CPU fallback)");
   }
   ie_status st = build_twiddles(c);
+  if (!st && c->layered) st = build_layer_table(c, bg->table);
   if (!st) {
     GreenSpec gs;
-    st = build_green(c, g->nx, g->ny, g->nz, &gs);
+    st = c->layered ? build_layer_spec(c, g->nx, g->ny, g->nz, 0, &gs) : build_green(c, g->nx, g->ny, g->nz, &gs);
     if (!st) c->greens.push_back(gs);
   }
   if (st) {
@@ -184,7 +202,11 @@ ie_status ie_destroy(ie_ctx* c) {
   if (!c) return IE_OK;
   if (c->stream) cudaStreamSynchronize(c->stream);
   else cudaDeviceSynchronize();
-  for (auto& g : c->greens) cudaFree(g.oct);
+  for (auto& g : c->greens) {
+    cudaFree(g.oct);
+    cudaFree(g.mhat);
+  }
+  cudaFree(c->tab);
   cudaFree(c->dsig);
   cudaFree(c->e0);
   cudaFree(c->tw.dev);
@@ -224,6 +246,8 @@ ie_status ie_set_contrast(ie_ctx* c, const void* sigma_dev, int32_t layout) {
 
 ie_status ie_set_source(ie_ctx* c, int32_t n_src, const double* pos, const double* moment) {
   if (!c || n_src < 1 || !pos || !moment) return fail(c, IE_ERR_INVALID_ARGUMENT, "set_source: bad arguments");
+  if (c->lay_sigma.size() > 1)
+    return fail(c, IE_ERR_UNSUPPORTED, "set_source: the layered E0 is caller-supplied (ie_set_incident)");
   const long long N = ncell(c);
   if (c->e0 && c->n_src != n_src) {
     cudaFree(c->e0);
@@ -302,7 +326,7 @@ ie_status ie_solve_subdomain(ie_ctx* c, const ie_box* box, int32_t nrhs, const v
                               o->min_iters});
   Arena ar = arena_of(c);
   std::vector<GmresResult> res;
-  ie_status st = gmres_batched(c, ar, bx, by, bz, (long long)c->g.nx * c->g.ny, c->g.nx, sys, o->restart,
+  ie_status st = gmres_batched(c, ar, bx, by, bz, b.k0, (long long)c->g.nx * c->g.ny, c->g.nx, sys, o->restart,
                                o->max_iters, res, nullptr);
   if (st) return st;
   IE_CUDA(c, cudaStreamSynchronize(c->stream));
@@ -346,7 +370,7 @@ ie_status ie_solve_dd(ie_ctx* c, const ie_dd_opts* o, void* e_dev, int32_t init_
       sys.push_back(GmresSystem{c->e0 + r * len, E + r * len, c->dsig, o->outer_tol, o->inner.min_iters});
     std::vector<GmresResult> res;
     long long ap = 0;
-    ie_status st = gmres_batched(c, ar, c->g.nx, c->g.ny, c->g.nz, (long long)c->g.nx * c->g.ny, c->g.nx, sys, m,
+    ie_status st = gmres_batched(c, ar, c->g.nx, c->g.ny, c->g.nz, 0, (long long)c->g.nx * c->g.ny, c->g.nx, sys, m,
                                  o->inner.max_iters, res, &ap);
     if (st) return st;
     bool allc = true, brk = false;
@@ -479,7 +503,7 @@ ie_status ie_solve_dd(ie_ctx* c, const ie_dd_opts* o, void* e_dev, int32_t init_
     std::vector<GmresResult> res;
     const size_t mark = ar.used;
     long long ap = 0;
-    ie_status s2 = gmres_batched(c, ar, b0.i1 - b0.i0, b0.j1 - b0.j0, b0.k1 - b0.k0, (long long)c->g.nx * c->g.ny,
+    ie_status s2 = gmres_batched(c, ar, b0.i1 - b0.i0, b0.j1 - b0.j0, b0.k1 - b0.k0, b0.k0, (long long)c->g.nx * c->g.ny,
                                  c->g.nx, sys, m, o->inner.max_iters, res, &ap);
     ar.used = mark;
     if (s2) return s2;
@@ -495,7 +519,7 @@ ie_status ie_solve_dd(ie_ctx* c, const ie_dd_opts* o, void* e_dev, int32_t init_
   std::map<std::vector<int>, std::vector<int>> groups;
   for (int i = 0; i < M; ++i) {
     const ie_box& b = o->boxes[i];
-    groups[{b.i1 - b.i0, b.j1 - b.j0, b.k1 - b.k0}].push_back(i);
+    groups[{b.i1 - b.i0, b.j1 - b.j0, b.k1 - b.k0, c->layered ? b.k0 : 0}].push_back(i);
   }
 
   int sweep = 0;
@@ -567,6 +591,8 @@ ie_status ie_receiver_fields(ie_ctx* c, const void* e_dev, int32_t n_rx, const d
                              void* v_host) {
   if (!c || !e_dev || n_rx < 1 || !rx_pos || !h_host) return fail(c, IE_ERR_INVALID_ARGUMENT, "receiver_fields: bad arguments");
   if (!c->contrast_set || c->n_src < 1) return fail(c, IE_ERR_STATE, "receiver_fields needs contrast and sources");
+  if (c->lay_sigma.size() > 1)
+    return fail(c, IE_ERR_UNSUPPORTED, "receiver_fields: layered backgrounds use ie_receiver_fields_table");
   if ((int)c->src_pos.size() != 3 * c->n_src)
     return fail(c, IE_ERR_STATE, "receiver_fields needs dipole sources (ie_set_source) for H0");
   Arena ar = arena_of(c);
@@ -627,10 +653,42 @@ ie_status ie_get_green_octant(ie_ctx* c, const ie_box* box, void* host_out) {
   std::string why;
   if (!box_ok(c, b, &why)) return fail(c, IE_ERR_INVALID_ARGUMENT, why);
   ie_status st;
-  const GreenSpec* gs = green_for(c, b.i1 - b.i0, b.j1 - b.j0, b.k1 - b.k0, &st);
+  if (c->layered) return fail(c, IE_ERR_STATE, "get_green_octant: layered context (ie_get_layer_spectrum)");
+  const GreenSpec* gs = green_for(c, b.i1 - b.i0, b.j1 - b.j0, b.k1 - b.k0, b.k0, &st);
   if (!gs) return st;
   const size_t n = 6ull * (gs->nx + 1) * (gs->ny + 1) * (gs->nz + 1);
   IE_CUDA(c, cudaMemcpyAsync(host_out, gs->oct, n * sizeof(double2), cudaMemcpyDeviceToHost, c->stream));
+  IE_CUDA(c, cudaStreamSynchronize(c->stream));
+  return IE_OK;
+}
+
+ie_status ie_receiver_fields_table(ie_ctx* c, const void* e_dev, int32_t n_rxdip, const void* e0rx_dev,
+                                   const void* h0_host, void* h_host) {
+  if (!c || !e_dev || n_rxdip < 1 || !e0rx_dev || !h0_host || !h_host)
+    return fail(c, IE_ERR_INVALID_ARGUMENT, "receiver_fields_table: bad arguments");
+  if (!c->contrast_set || c->n_src < 1) return fail(c, IE_ERR_STATE, "receiver_fields_table needs contrast and sources");
+  Arena ar = arena_of(c);
+  const size_t pairs = (size_t)c->n_src * n_rxdip;
+  const size_t avail = c->ws_bytes > 4096 ? (c->ws_bytes - 4096) / sizeof(double2) : 0;
+  const size_t elems = std::min(pairs * 256, avail);
+  double2* scratch = elems >= pairs ? (double2*)ar.take(elems * sizeof(double2)) : nullptr;
+  if (!scratch) return fail(c, IE_ERR_OUT_OF_MEMORY, "workspace too small for receivers");
+  return receivers_table(c, (const double2*)e_dev, n_rxdip, (const double2*)e0rx_dev, (const cplx*)h0_host,
+                         (cplx*)h_host, scratch, elems);
+}
+
+ie_status ie_get_layer_spectrum(ie_ctx* c, const ie_box* box, void* host_out) {
+  if (!c || !host_out) return fail(c, IE_ERR_INVALID_ARGUMENT, "get_layer_spectrum: bad arguments");
+  if (!c->layered) return fail(c, IE_ERR_STATE, "get_layer_spectrum: homogeneous context (ie_get_green_octant)");
+  const ie_box b = box ? *box : full_box(c);
+  std::string why;
+  if (!box_ok(c, b, &why)) return fail(c, IE_ERR_INVALID_ARGUMENT, why);
+  ie_status st;
+  const GreenSpec* gs = green_for(c, b.i1 - b.i0, b.j1 - b.j0, b.k1 - b.k0, b.k0, &st);
+  if (!gs) return st;
+  const size_t R = 3ull * gs->nz;
+  const size_t n = (size_t)(gs->nx + 1) * (gs->ny + 1) * R * R;
+  IE_CUDA(c, cudaMemcpyAsync(host_out, gs->mhat, n * sizeof(double2), cudaMemcpyDeviceToHost, c->stream));
   IE_CUDA(c, cudaStreamSynchronize(c->stream));
   return IE_OK;
 }

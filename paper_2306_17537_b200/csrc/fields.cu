@@ -20,9 +20,11 @@ static inline unsigned grid_for(long long n, int block, int cap = 148 * 16) {
 
 // ------------------------------------------------------------------- contrast
 // FULL9 cell-major [N][3][3] -> dsigma SYM6 SoA [6][N] = sigma - sigma_b I; flags asymmetry.
-__global__ void k_contrast_full9(const double* __restrict__ s, double* __restrict__ ds, long long N, double sb,
-                                 int* __restrict__ bad) {
+// sbz (layered backgrounds): sigma_b of each cell layer, indexed c / nxy; else sb for all
+__global__ void k_contrast_full9(const double* __restrict__ s, double* __restrict__ ds, long long N, double sb0,
+                                 const double* __restrict__ sbz, long long nxy, int* __restrict__ bad) {
   for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < N; c += (long long)gridDim.x * blockDim.x) {
+    const double sb = sbz ? sbz[c / nxy] : sb0;
     const double* m = s + 9 * c;
     const double xx = m[0], xy = m[1], xz = m[2], yx = m[3], yy = m[4], yz = m[5], zx = m[6], zy = m[7], zz = m[8];
     const double mx = fmax(fmax(fabs(xx), fabs(yy)), fmax(fabs(zz), fmax(fabs(xy), fmax(fabs(xz), fabs(yz)))));
@@ -36,9 +38,10 @@ __global__ void k_contrast_full9(const double* __restrict__ s, double* __restric
     ds[5 * N + c] = yz;
   }
 }
-__global__ void k_contrast_sym6(const double* __restrict__ s, double* __restrict__ ds, long long N, double sb,
-                                int* __restrict__ bad) {
+__global__ void k_contrast_sym6(const double* __restrict__ s, double* __restrict__ ds, long long N, double sb0,
+                                const double* __restrict__ sbz, long long nxy, int* __restrict__ bad) {
   for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < N; c += (long long)gridDim.x * blockDim.x) {
+    const double sb = sbz ? sbz[c / nxy] : sb0;
     for (int k = 0; k < 6; ++k) {
       const double v = s[k * N + c];
       if (!isfinite(v)) atomicOr(bad, 1);
@@ -51,12 +54,22 @@ ie_status pack_contrast(ie_ctx* c, const void* sigma_dev, int layout) {
   const long long N = (long long)c->g.nx * c->g.ny * c->g.nz;
   if (!c->dsig) IE_CUDA(c, cudaMalloc(&c->dsig, 6 * N * sizeof(double)));
   int* bad = nullptr;
-  IE_CUDA(c, cudaMalloc(&bad, sizeof(int)));
+  double* sbz = nullptr;  // per-layer background (P:48 with sigma_b(z); reading R17)
+  IE_CUDA(c, cudaMalloc(&bad, 8 + (c->layered ? c->g.nz * sizeof(double) : 0)));
   IE_CUDA(c, cudaMemsetAsync(bad, 0, sizeof(int), c->stream));
+  std::vector<double> hsb;
+  if (c->layered) {
+    for (int k = 0; k < c->g.nz; ++k) hsb.push_back(sigma_b_at(c, k));
+    sbz = (double*)((char*)bad + 8);
+    IE_CUDA(c, cudaMemcpyAsync(sbz, hsb.data(), hsb.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  }
+  const long long nxy = (long long)c->g.nx * c->g.ny;
   if (layout == 0)
-    k_contrast_full9<<<grid_for(N, 256), 256, 0, c->stream>>>((const double*)sigma_dev, c->dsig, N, c->sigma_b, bad);
+    k_contrast_full9<<<grid_for(N, 256), 256, 0, c->stream>>>((const double*)sigma_dev, c->dsig, N, c->sigma_b, sbz,
+                                                              nxy, bad);
   else
-    k_contrast_sym6<<<grid_for(N, 256), 256, 0, c->stream>>>((const double*)sigma_dev, c->dsig, N, c->sigma_b, bad);
+    k_contrast_sym6<<<grid_for(N, 256), 256, 0, c->stream>>>((const double*)sigma_dev, c->dsig, N, c->sigma_b, sbz,
+                                                             nxy, bad);
   c->launches++;
   int hbad = 0;
   cudaError_t e = cudaGetLastError();

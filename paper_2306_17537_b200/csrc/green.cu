@@ -13,23 +13,9 @@
 
 #include "fft_core.cuh"
 #include "ie_internal.h"
+#include "kernel_eval.cuh"
 
 namespace ie {
-
-struct GreenArgs {
-  int nx, ny, nz;
-  double dx, dy, dz, dv;
-  double k0r, k0i, sigma_b;
-  double selfr, selfi;
-};
-
-// complex helpers on (re, im) doubles
-__device__ __forceinline__ double2 cexp_i(double2 z) {  // exp(i z)
-  const double m = exp(-z.y);
-  double s, c;
-  sincos(z.x, &s, &c);
-  return make_double2(m * c, m * s);
-}
 
 // K_comp at circulant index (ix,iy,iz) of the (2nx,2ny,2nz) grid, comp in 0..5
 __global__ void k_green_sample(double2* __restrict__ C, GreenArgs a, int comp) {
@@ -43,37 +29,7 @@ __global__ void k_green_sample(double2* __restrict__ C, GreenArgs a, int comp) {
       const int dxi = ix < a.nx ? ix : ix - (int)Lx;
       const int dyi = iy < a.ny ? iy : iy - (int)Ly;
       const int dzi = iz < a.nz ? iz : iz - (int)Lz;
-      if (dxi == 0 && dyi == 0 && dzi == 0) {
-        if (comp < 3) out = make_double2(a.selfr, a.selfi);
-      } else {
-        const double X = dxi * a.dx, Y = dyi * a.dy, Z = dzi * a.dz;
-        const double R = sqrt(X * X + Y * Y + Z * Z);
-        const double iR = 1.0 / R;
-        // g = exp(i k0 R) / (4 pi R)
-        const double2 e1 = cexp_i(make_double2(a.k0r * R, a.k0i * R));
-        const double2 g = make_double2(e1.x * iR / (4.0 * kPi), e1.y * iR / (4.0 * kPi));
-        // k0^2, i k0 / R
-        const double2 k2 = make_double2(a.k0r * a.k0r - a.k0i * a.k0i, 2.0 * a.k0r * a.k0i);
-        const double2 ikR = make_double2(-a.k0i * iR, a.k0r * iR);
-        // alpha = k0^2 + i k0/R - 1/R^2 ; beta = 3/R^2 - 3 i k0/R - k0^2
-        const double2 al = make_double2(k2.x + ikR.x - iR * iR, k2.y + ikR.y);
-        const double2 be = make_double2(3.0 * iR * iR - 3.0 * ikR.x - k2.x, -3.0 * ikR.y - k2.y);
-        double hp, hq;
-        const double hx = X * iR, hy = Y * iR, hz = Z * iR;
-        bool diag = comp < 3;
-        switch (comp) {
-          case 0: hp = hx; hq = hx; break;
-          case 1: hp = hy; hq = hy; break;
-          case 2: hp = hz; hq = hz; break;
-          case 3: hp = hx; hq = hy; break;
-          case 4: hp = hx; hq = hz; break;
-          default: hp = hy; hq = hz; break;
-        }
-        double2 coef = make_double2(be.x * hp * hq, be.y * hp * hq);
-        if (diag) coef = make_double2(coef.x + al.x, coef.y + al.y);
-        const double s = a.dv / a.sigma_b;
-        out = make_double2((coef.x * g.x - coef.y * g.y) * s, (coef.x * g.y + coef.y * g.x) * s);
-      }
+      out = kernel_sample(a, dxi, dyi, dzi, comp);
     }
     C[e] = out;
   }
@@ -141,7 +97,7 @@ static cudaError_t fft_axis_launch(double2* data, long long inner, long long out
   return cudaGetLastError();
 }
 
-static cudaError_t fft_axis(int L, double2* data, long long inner, long long outer, const double2* tw,
+cudaError_t fft_axis(int L, double2* data, long long inner, long long outer, const double2* tw,
                             cudaStream_t s) {
   switch (L) {
     case 2: return fft_axis_launch<2>(data, inner, outer, tw, s);
@@ -158,7 +114,7 @@ static cudaError_t fft_axis(int L, double2* data, long long inner, long long out
   return cudaErrorInvalidValue;
 }
 
-ie_status build_green(ie_ctx* c, int nx, int ny, int nz, GreenSpec* out) {
+GreenArgs green_args(const ie_ctx* c, int nx, int ny, int nz) {
   GreenArgs a;
   a.nx = nx;
   a.ny = ny;
@@ -172,6 +128,11 @@ ie_status build_green(ie_ctx* c, int nx, int ny, int nz, GreenSpec* out) {
   a.sigma_b = c->sigma_b;
   a.selfr = c->self.real();
   a.selfi = c->self.imag();
+  return a;
+}
+
+ie_status build_green(ie_ctx* c, int nx, int ny, int nz, GreenSpec* out) {
+  const GreenArgs a = green_args(c, nx, ny, nz);
   const long long Lx = 2 * nx, Ly = 2 * ny, Lz = 2 * nz, total = Lx * Ly * Lz;
   const long long ooct = (long long)(nx + 1) * (ny + 1) * (nz + 1);
   out->nx = nx;
@@ -202,12 +163,13 @@ ie_status build_green(ie_ctx* c, int nx, int ny, int nz, GreenSpec* out) {
   return IE_OK;
 }
 
-const GreenSpec* green_for(ie_ctx* c, int nx, int ny, int nz, ie_status* st) {
+const GreenSpec* green_for(ie_ctx* c, int nx, int ny, int nz, int k0, ie_status* st) {
   *st = IE_OK;
+  if (!c->layered) k0 = 0;  // homogeneous spectra depend on the shape only
   for (auto& g : c->greens)
-    if (g.nx == nx && g.ny == ny && g.nz == nz) return &g;
+    if (g.nx == nx && g.ny == ny && g.nz == nz && g.k0 == k0) return &g;
   GreenSpec gs;
-  *st = build_green(c, nx, ny, nz, &gs);
+  *st = c->layered ? build_layer_spec(c, nx, ny, nz, k0, &gs) : build_green(c, nx, ny, nz, &gs);
   if (*st != IE_OK) return nullptr;
   c->greens.push_back(gs);
   return &c->greens.back();

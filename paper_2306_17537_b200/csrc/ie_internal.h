@@ -46,6 +46,7 @@ struct ApplyParams {
   const double2* tw_z;   // L = 2nz, forward order
   const double2* tw_zr;  // L = 2nz, reversed order
   const double2* pw_z;   // exp(-2 pi i m / 2nz), m < 2nz (radix-16 z-pass)
+  const double2* mhat;   // layered background: packed z-z' spectra (layered.cu), else null
   int n_items;
   ApplyItem items[kMaxItems];
 };
@@ -60,7 +61,9 @@ struct Twiddles {
 
 struct GreenSpec {
   int nx, ny, nz;
-  double2* oct = nullptr;  // [6][nz+1][ny+1][nx+1]
+  int k0 = 0;               // layered: first cell layer of the domain (the spectra depend on it)
+  double2* oct = nullptr;   // homogeneous: [6][nz+1][ny+1][nx+1]
+  double2* mhat = nullptr;  // layered: [(ny+1)(nx+1)][3nz (q,k')][3nz (p,k)] (layered.cu)
 };
 
 // workspace bump allocator (caller-owned memory)
@@ -81,6 +84,12 @@ struct ie_ctx {
   ie::Twiddles tw;
   std::deque<ie::GreenSpec> greens;  // [0] = whole grid (deque: stable element addresses)
   double* dsig = nullptr;             // sym6 [6][nz][ny][nx]
+  // layered background (readings R17-R19): table of kernel samples on the
+  // device, quadrant offsets [9][nz][nz][ny][nx]; per-layer conductivities
+  bool layered = false;
+  int table_format = 0;
+  std::vector<double> lay_sigma, lay_z;  // [n_layers], [n_layers-1]
+  double2* tab = nullptr;
   double2* e0 = nullptr;
   int n_src = 0;
   std::vector<double> src_pos, src_mom;  // host copies of the dipoles (for H0 at receivers)
@@ -132,7 +141,17 @@ ie_status launch_apply(ie_ctx* c, ApplyParams& p);  // p.items/n_items may excee
 size_t apply_scratch_bytes(int nx, int ny, int nz, int n_items);
 // green.cu
 ie_status build_green(ie_ctx* c, int nx, int ny, int nz, GreenSpec* out);
-const GreenSpec* green_for(ie_ctx* c, int nx, int ny, int nz, ie_status* st);
+// the spectra of a domain of (nx,ny,nz) cells starting at cell layer k0 (k0 only matters
+// for layered backgrounds)
+const GreenSpec* green_for(ie_ctx* c, int nx, int ny, int nz, int k0, ie_status* st);
+cudaError_t fft_axis(int L, double2* data, long long inner, long long outer, const double2* tw, cudaStream_t s);
+// layered.cu
+ie_status build_layer_table(ie_ctx* c, const void* host_table);
+ie_status build_layer_spec(ie_ctx* c, int nx, int ny, int nz, int k0, GreenSpec* out);
+cudaError_t launch_zlayer(const ApplyParams& p, cudaStream_t s);
+ie_status receivers_table(ie_ctx* c, const double2* e, int n_rx, const double2* e0rx, const cplx* h0, cplx* out,
+                          double2* scratch, size_t scratch_elems);
+double sigma_b_at(const ie_ctx* c, int k);  // background conductivity of cell layer k
 // fields.cu
 ie_status pack_contrast(ie_ctx* c, const void* sigma_dev, int layout);
 ie_status compute_incident(ie_ctx* c, int n_src, const double* pos, const double* moment, double2* out);
@@ -158,7 +177,7 @@ struct GmresResult {
   int iters = 0, restarts = 0, converged = 0, breakdown = 0;
   double relres_est = 0, relres_true = 0;
 };
-ie_status gmres_batched(ie_ctx* c, Arena& ar, int nx, int ny, int nz, long long ds_zs, long long ds_ys,
+ie_status gmres_batched(ie_ctx* c, Arena& ar, int nx, int ny, int nz, int k0, long long ds_zs, long long ds_ys,
                         const std::vector<GmresSystem>& sys, int restart, int max_iters,
                         std::vector<GmresResult>& res, long long* applies);
 size_t gmres_scratch_bytes(int nx, int ny, int nz, int nsys, int restart);

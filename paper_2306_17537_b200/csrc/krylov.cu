@@ -154,7 +154,7 @@ struct SysState {
 
 }  // namespace
 
-ie_status gmres_batched(ie_ctx* c, Arena& ar, int nx, int ny, int nz, long long ds_zs, long long ds_ys,
+ie_status gmres_batched(ie_ctx* c, Arena& ar, int nx, int ny, int nz, int k0, long long ds_zs, long long ds_ys,
                         const std::vector<GmresSystem>& sys, int m, int max_iters, std::vector<GmresResult>& res,
                         long long* applies) {
   const int S = (int)sys.size();
@@ -164,7 +164,7 @@ ie_status gmres_batched(ie_ctx* c, Arena& ar, int nx, int ny, int nz, long long 
   const int items = std::min(S, kMaxItems);
   const int nblk = dot_blocks(S);
   ie_status st;
-  const GreenSpec* gs = green_for(c, nx, ny, nz, &st);
+  const GreenSpec* gs = green_for(c, nx, ny, nz, k0, &st);
   if (!gs) return st;
   // staging (host pinned + device mirror): [dot jobs S*64 | axpy jobs S*64 | coefs S*(m+2)*16]
   const size_t jobs_bytes = (size_t)S * 64 * 2 + (size_t)S * (m + 2) * sizeof(double2);
@@ -203,6 +203,7 @@ ie_status gmres_batched(ie_ctx* c, Arena& ar, int nx, int ny, int nz, long long 
   ap.ds_zs = ds_zs;
   ap.ds_ys = ds_ys;
   ap.ghat = gs->oct;
+  ap.mhat = gs->mhat;
   ap.X1 = scratch;
   ap.X2 = scratch + (size_t)items * 3 * 2 * N;
   // apply to a list of (system, input, output) with given coefficients

@@ -702,7 +702,9 @@ static cudaError_t run_apply(const ApplyParams& p, cudaStream_t s, cudaEvent_t* 
   IE_DISPATCH_L(2 * p.ny, wrap_yfwd, &e, p, s, max_planes);
   if (e) return e;
   mark(2);
-  if (const int W16 = zconv16_width(2 * p.nz, 2 * p.nx)) {
+  if (p.mhat) {  // layered background: z-z' contraction per horizontal wavenumber (layered.cu)
+    e = launch_zlayer(p, s);
+  } else if (const int W16 = zconv16_width(2 * p.nz, 2 * p.nx)) {
     e = go_zconv16(p, s, W16);
   } else {
     IE_DISPATCH_L(2 * p.nz, wrap_zconv, &e, p, s);

@@ -133,10 +133,11 @@ def test_dd_zero_contrast_zero_sweeps():
 
 
 @pytest.mark.parametrize("scheme", ["full", "jacobi", "gauss_seidel"])
-def test_c2capped_solves_match_oracle_gmres(scheme):
-    """c2-capped (32^3, 2 z-boxes): GPU at tol 1e-9 vs oracle full-domain GMRES at 1e-12."""
+def test_c2mod_solves_match_oracle_gmres(scheme):
+    """c2mod (the c2 geometry, 32^3, 2 z-boxes, moderate contrast): GPU at tol 1e-9 vs oracle
+    full-domain GMRES at 1e-12."""
     import paper_2306_17537_b200 as ie
-    cfg = make_config("c2capped")
+    cfg = make_config("c2mod")
     ctx, sigma = gpu_ctx(cfg)
     k0, ds, E0 = oracle_setup(cfg, sigma)
     Aop = op.Operator(cfg.n, cfg.hvec, k0, cfg.sigma_b, ds)

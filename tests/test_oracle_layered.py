@@ -138,3 +138,18 @@ def test_layered_dd_converges_to_dense_lu(scheme):
     E, st = dd.solve_dd(sysl, E0, scheme, outer_tol=1e-11, restart=30)
     assert st["converged"]
     assert np.linalg.norm(E - X) < 1e-8 * np.linalg.norm(X)
+
+
+def test_spectrum_mirror_relation_on_arbitrary_tables():
+    """M(2n - kx) = Dx M(kx) Dx and M(2n - ky) = Dy M(ky) Dy (D = diag of the mirror signs): the
+    structure the GPU z-contraction relies on to serve 4 wavenumbers from one matrix."""
+    n = (8, 4, 3)
+    nx, ny, nz = n
+    M = lay.layered_spectra(lay.random_table(n, np.random.default_rng(12)))
+    for ix, iy in [(1, 1), (3, 2), (0, 3), (4, 0)]:
+        a = M[..., iy, (2 * nx - ix) % (2 * nx)]
+        b = np.einsum("p,q,pqkl->pqkl", lay.SX, lay.SX, M[..., iy, ix])
+        assert np.abs(a - b).max() < 1e-15 * np.abs(M).max()
+        a = M[..., (2 * ny - iy) % (2 * ny), ix]
+        b = np.einsum("p,q,pqkl->pqkl", lay.SY, lay.SY, M[..., iy, ix])
+        assert np.abs(a - b).max() < 1e-15 * np.abs(M).max()
