@@ -58,3 +58,11 @@ __device__ __forceinline__ void prefetch_l2(const void* p) {
 }
 
 }  // namespace ie
+
+namespace ie {
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+}  // namespace ie

@@ -16,9 +16,12 @@
 // M (the full-spectrum matrix at a mirrored wavenumber is D M D, D = diag(sx, sy, 1)).
 #include <math.h>
 
+#include <stdlib.h>
+
 #include <algorithm>
 #include <vector>
 
+#include "bulk_copy.cuh"
 #include "fft_core.cuh"
 #include "ie_internal.h"
 #include "kernel_eval.cuh"
@@ -205,6 +208,217 @@ __global__ void __launch_bounds__(256) k_zlayer(const __grid_constant__ ApplyPar
   }
 }
 
+// The same contraction on the FP64 tensor cores (DMMA, mma.sync m8n8k4 f64) when the
+// right-hand sides make it a real contraction (NI >= 2: 4 NI >= 8 columns, one n-tile per 8)
+// and 3nz is a multiple of 8.  A = M (rows (p,k), cols (q,k')), B = X (rows (q,k'), cols =
+// column slots), complex as four real MMAs per (k-step, n-tile).  Fragments (PTX m8n8k4 f64):
+// lane l holds A[l/4][l%4], B[l%4][l/4], C[l/4][2(l%4) + {0,1}].  Each warp owns 8-row tiles
+// and streams its rows of M with 16-byte loads (8 consecutive rows x 4 k: 128-byte segments).
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+template <int NI>
+__global__ void __launch_bounds__(256) k_zlayer_mma(const __grid_constant__ ApplyParams p) {
+  constexpr int NS = 4 * NI, NT = (NS + 7) / 8, NSP = NT * 8;
+  extern __shared__ __align__(16) double2 xs[];  // [R][NSP], signs applied, zero padded
+  const int nx = p.nx, ny = p.ny, nz = p.nz, Lx = 2 * nx, Ly = 2 * ny, R = 3 * nz;
+  const int ixy = blockIdx.x, ix = ixy % (nx + 1), iy = ixy / (nx + 1);
+  const int kxs[2] = {ix, Lx - ix}, kys[2] = {iy, Ly - iy};
+  const int nkx = (ix == 0 || ix == nx) ? 1 : 2, nky = (iy == 0 || iy == ny) ? 1 : 2;
+  const long long cs = (long long)nz * Ly * Lx, zs = (long long)Ly * Lx;
+  const int z0 = p.items[0].sz0, z1 = p.items[0].sz1;
+  for (int e = threadIdx.x; e < R * NSP; e += blockDim.x) {
+    const int slot = e % NSP, row = e / NSP, q = row / nz, kp = row % nz;
+    const int item = slot % NI, cc = slot / NI, cx = cc & 1, cy = cc >> 1;
+    double2 v = czero();
+    if (slot < NS && item < p.n_items && cx < nkx && cy < nky && kp >= z0 && kp < z1) {
+      v = p.X2[(long long)item * 3 * cs + q * cs + kp * zs + (long long)kys[cy] * Lx + kxs[cx]];
+      if ((q == 0 && cx == 1) || (q == 1 && cy == 1)) v = make_double2(-v.x, -v.y);
+    }
+    xs[e] = v;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  const int ar = lane >> 2, ac = lane & 3;  // A[ar][ac], B[ac][ar], C[ar][2 ac + j]
+  const double2* M = p.mhat + (long long)ixy * R * R;
+  for (int rt = warp; rt < R / 8; rt += nwarps) {
+    const int r0 = rt * 8;
+    double cr[NT][2], ci[NT][2];
+#pragma unroll
+    for (int t = 0; t < NT; ++t) cr[t][0] = cr[t][1] = ci[t][0] = ci[t][1] = 0.0;
+    const double2* Ma = M + (long long)ac * R + r0 + ar;
+#pragma unroll 4
+    for (int k0 = 0; k0 < R; k0 += 4) {
+      const double2 a = __ldg(Ma + (long long)k0 * R);
+      const double nai = -a.y;
+#pragma unroll
+      for (int t = 0; t < NT; ++t) {
+        const double2 b = xs[(k0 + ac) * NSP + t * 8 + ar];
+        dmma(cr[t][0], cr[t][1], a.x, b.x);
+        dmma(cr[t][0], cr[t][1], nai, b.y);
+        dmma(ci[t][0], ci[t][1], a.x, b.y);
+        dmma(ci[t][0], ci[t][1], a.y, b.x);
+      }
+    }
+    const int pk = r0 + ar, pp = pk / nz, k = pk % nz;
+#pragma unroll
+    for (int t = 0; t < NT; ++t)
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int s = t * 8 + 2 * ac + j;
+        const int item = s % NI, cc = s / NI, cx = cc & 1, cy = cc >> 1;
+        if (s < NS && item < p.n_items && cx < nkx && cy < nky) {
+          double2 v = make_double2(cr[t][j], ci[t][j]);
+          if ((pp == 0 && cx == 1) || (pp == 1 && cy == 1)) v = make_double2(-v.x, -v.y);
+          p.X2[(long long)item * 3 * cs + pp * cs + k * zs + (long long)kys[cy] * Lx + kxs[cx]] = v;
+        }
+      }
+  }
+}
+
+// Warp-specialised version: a producer warp streams M(ix,iy) into a 2-stage shared ring with
+// bulk asynchronous copies (TMA bulk mode, one 8-row chunk = 8*3nz*16 contiguous bytes per
+// copy, completion on mbarriers); 8 consumer warps feed the DMMA tensor cores from shared
+// memory and release each stage through an "empty" mbarrier, so HBM streaming is decoupled
+// from the tensor-core work.  Complex arithmetic without padding: B is X viewed as real
+// columns (Re X_s, Im X_s interleaved, 2*4NI columns = NI n-tiles of 8), and per k-step
+// C1 += Re(M) B, C2 += Im(M) B; a lane's C pair (2j, 2j+1) is (Re X_s, Im X_s) of one slot,
+// so Y_s = (C1[2s] - C2[2s+1]) + i (C1[2s+1] + C2[2s]) in registers.
+template <int NI, int RT>
+__global__ void __launch_bounds__(288, 2) k_zlayer_tma(const __grid_constant__ ApplyParams p) {
+  constexpr int NS = 4 * NI, NT = NI;      // slots; real columns 2 NS = 8 NI: NI n-tiles
+  constexpr int KC = 8, NST = 2, NCW = 8;  // k-rows per chunk, ring stages, consumer warps
+  extern __shared__ __align__(128) double2 smem[];
+  const int nx = p.nx, ny = p.ny, nz = p.nz, Lx = 2 * nx, Ly = 2 * ny, R = 3 * nz;
+  double2* xs = smem;                     // [R][NS] complex = [R][2NS] real
+  const double* xd = reinterpret_cast<const double*>(xs);
+  double2* ring = smem + R * NS;          // [NST][KC][R]
+  uint64_t* full = reinterpret_cast<uint64_t*>(ring + NST * KC * R);
+  uint64_t* empty = full + NST;
+  const int ixy = blockIdx.x, ix = ixy % (nx + 1), iy = ixy / (nx + 1);
+  const int kxs[2] = {ix, Lx - ix}, kys[2] = {iy, Ly - iy};
+  const int nkx = (ix == 0 || ix == nx) ? 1 : 2, nky = (iy == 0 || iy == ny) ? 1 : 2;
+  const long long cs = (long long)nz * Ly * Lx, zs = (long long)Ly * Lx;
+  const int z0 = p.items[0].sz0, z1 = p.items[0].sz1;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nchunks = R / KC;
+  const double2* M = p.mhat + (long long)ixy * R * R;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < NST; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], NCW);
+    }
+  }
+  __syncthreads();
+  if (warp == NCW) {  // ---- producer
+    if (lane == 0) {
+      for (int ch = 0; ch < nchunks; ++ch) {
+        const int st = ch % NST;
+        if (ch >= NST) mbar_wait(&empty[st], ((ch / NST) - 1) & 1);
+        const uint32_t bytes = (uint32_t)(KC * R * sizeof(double2));
+        mbar_arrive_expect_tx(&full[st], bytes);
+        bulk_g2s(ring + st * KC * R, M + (long long)ch * KC * R, bytes, &full[st]);
+      }
+    }
+    return;
+  }
+  // ---- consumers: stage X (signs applied), then the DMMA loop
+  for (int e = threadIdx.x; e < R * NS; e += NCW * 32) {
+    const int slot = e % NS, row = e / NS, q = row / nz, kp = row % nz;
+    const int item = slot % NI, cc = slot / NI, cx = cc & 1, cy = cc >> 1;
+    double2 v = czero();
+    if (item < p.n_items && cx < nkx && cy < nky && kp >= z0 && kp < z1) {
+      v = p.X2[(long long)item * 3 * cs + q * cs + kp * zs + (long long)kys[cy] * Lx + kxs[cx]];
+      if ((q == 0 && cx == 1) || (q == 1 && cy == 1)) v = make_double2(-v.x, -v.y);
+    }
+    xs[e] = v;
+  }
+  asm volatile("bar.sync 1, %0;" ::"n"(NCW * 32));  // consumers only
+  const int ar = lane >> 2, ac = lane & 3;
+  double c1[RT][NT][2], c2[RT][NT][2];
+#pragma unroll
+  for (int r = 0; r < RT; ++r)
+#pragma unroll
+    for (int t = 0; t < NT; ++t) c1[r][t][0] = c1[r][t][1] = c2[r][t][0] = c2[r][t][1] = 0.0;
+  for (int ch = 0; ch < nchunks; ++ch) {
+    const int st = ch % NST;
+    mbar_wait(&full[st], (ch / NST) & 1);
+    const double2* A = ring + st * KC * R;
+#pragma unroll
+    for (int kk = 0; kk < KC; kk += 4) {
+      const int k0 = ch * KC + kk;
+      double b[NT];
+#pragma unroll
+      for (int t = 0; t < NT; ++t) b[t] = xd[(k0 + ac) * (2 * NS) + t * 8 + ar];
+#pragma unroll
+      for (int r = 0; r < RT; ++r) {
+        const double2 a = A[(kk + ac) * R + (warp + r * NCW) * 8 + ar];
+#pragma unroll
+        for (int t = 0; t < NT; ++t) {
+          dmma(c1[r][t][0], c1[r][t][1], a.x, b[t]);
+          dmma(c2[r][t][0], c2[r][t][1], a.y, b[t]);
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[st]);
+  }
+#pragma unroll
+  for (int r = 0; r < RT; ++r) {
+    const int pk = (warp + r * NCW) * 8 + ar, pp = pk / nz, k = pk % nz;
+#pragma unroll
+    for (int t = 0; t < NT; ++t) {
+      const int sl = t * 4 + ac;  // real columns 2 sl, 2 sl + 1
+      const int item = sl % NI, cc = sl / NI, cx = cc & 1, cy = cc >> 1;
+      if (item < p.n_items && cx < nkx && cy < nky) {
+        double2 v = make_double2(c1[r][t][0] - c2[r][t][1], c1[r][t][1] + c2[r][t][0]);
+        if ((pp == 0 && cx == 1) || (pp == 1 && cy == 1)) v = make_double2(-v.x, -v.y);
+        p.X2[(long long)item * 3 * cs + pp * cs + k * zs + (long long)kys[cy] * Lx + kxs[cx]] = v;
+      }
+    }
+  }
+}
+
+template <int NI, int RT>
+static cudaError_t go_zlayer_tma(const ApplyParams& p, cudaStream_t s) {
+  const int R = 3 * p.nz;
+  const size_t smem = (size_t)(R * 4 * NI + 2 * 8 * R) * sizeof(double2) + 4 * sizeof(uint64_t);
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute((const void*)k_zlayer_tma<NI, RT>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e) return e;
+  }
+  k_zlayer_tma<NI, RT><<<(p.nx + 1) * (p.ny + 1), 288, smem, s>>>(p);
+  return cudaGetLastError();
+}
+
+template <int NI>
+static cudaError_t go_zlayer_tma_r(const ApplyParams& p, cudaStream_t s) {
+  // row tiles per consumer warp: R / 8 tiles over 8 warps
+  const int tiles = 3 * p.nz / 8;
+  switch (tiles) {
+    case 24: return go_zlayer_tma<NI, 3>(p, s);  // nz = 64
+    case 48: return go_zlayer_tma<NI, 6>(p, s);  // nz = 128
+  }
+  return cudaErrorInvalidValue;
+}
+
+template <int NI>
+static cudaError_t go_zlayer_mma(const ApplyParams& p, cudaStream_t s) {
+  constexpr int NSP = ((4 * NI + 7) / 8) * 8;
+  const size_t smem = (size_t)3 * p.nz * NSP * sizeof(double2);
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute((const void*)k_zlayer_mma<NI>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e) return e;
+  }
+  k_zlayer_mma<NI><<<(p.nx + 1) * (p.ny + 1), 256, smem, s>>>(p);
+  return cudaGetLastError();
+}
+
 template <int NI>
 static cudaError_t go_zlayer(const ApplyParams& p, cudaStream_t s) {
   const size_t smem = (size_t)3 * p.nz * 4 * NI * sizeof(double2);
@@ -219,17 +433,36 @@ static cudaError_t go_zlayer(const ApplyParams& p, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-// items of one launch share M (same domain); up to 4 per CTA, more by repeated launches
+// IE_ZLAYER_MODE (side-by-side measurement): 0 (default) TMA ring + DMMA, 1 DMMA with direct
+// loads, 2 DFMA
+static int zlayer_mode() {
+  static const int v = [] {
+    const char* e = getenv("IE_ZLAYER_MODE");
+    return e ? atoi(e) : 0;
+  }();
+  return v;
+}
+
+// items of one launch share M (same domain); up to 3 (DMMA) or 4 (DFMA) per CTA, more by
+// repeated launches
 cudaError_t launch_zlayer(const ApplyParams& p, cudaStream_t s) {
   ApplyParams q = p;
-  for (int i0 = 0; i0 < p.n_items; i0 += 4) {
-    const int ni = std::min(4, p.n_items - i0);
+  const int group = (p.nz % 64 == 0 && zlayer_mode() == 0) ? 3 : 4;  // the DMMA kernel is best at <= 3
+  for (int i0 = 0; i0 < p.n_items; i0 += group) {
+    const int ni = std::min(group, p.n_items - i0);
     q.n_items = ni;
     for (int i = 0; i < ni; ++i) q.items[i] = p.items[i0 + i];
     const long long per_item = 3LL * p.nz * (2LL * p.ny) * (2LL * p.nx);
     q.X2 = p.X2 + (long long)i0 * per_item;
-    cudaError_t e = ni == 1 ? go_zlayer<1>(q, s) : ni == 2 ? go_zlayer<2>(q, s) : ni == 3 ? go_zlayer<3>(q, s)
-                                                                                          : go_zlayer<4>(q, s);
+    cudaError_t e;
+    const int mode = zlayer_mode();
+    if (p.nz % 64 == 0 && mode == 0)  // DMMA fed by the TMA ring (3nz/8 row tiles over 8 warps)
+      e = ni == 1 ? go_zlayer_tma_r<1>(q, s) : ni == 2 ? go_zlayer_tma_r<2>(q, s)
+                  : ni == 3 ? go_zlayer_tma_r<3>(q, s) : go_zlayer_tma_r<4>(q, s);
+    else if (ni >= 2 && p.nz % 8 == 0 && mode <= 1)  // DMMA, operands straight from global
+      e = ni == 2 ? go_zlayer_mma<2>(q, s) : ni == 3 ? go_zlayer_mma<3>(q, s) : go_zlayer_mma<4>(q, s);
+    else
+      e = ni == 1 ? go_zlayer<1>(q, s) : ni == 2 ? go_zlayer<2>(q, s) : ni == 3 ? go_zlayer<3>(q, s) : go_zlayer<4>(q, s);
     if (e) return e;
   }
   return cudaSuccess;
