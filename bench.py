@@ -176,6 +176,48 @@ def run_reference(args, cfg, sigma, rank, ws):
 
 
 # ------------------------------------------------------------------------------- ours
+def layered_leg(steps=10, name="c3h", nrhs=3):
+    """A3L: the c3 grid (64^3) and its contrast recipe through the layered-table path (K-C'
+    z-z' contraction on the FP64 tensor cores) with the library's degenerate equal-layer table
+    (table_format 2, sigma = 1 S/m, 400 kHz -- the physical 3-layer table is not built, DESIGN
+    R19), triaxial source = 3 right-hand sides.  Per-kernel CUDA-event times."""
+    import torch
+    import paper_2306_17537_b200 as ie
+    from ie_workloads import make_config
+    cfg = make_config(name)
+    ctx = ie.ie_create(cfg.n, cfg.hvec, cfg.origin, cfg.sigma_b, cfg.freq, table_format=2)
+    ie.ensure_workspace(ctx, nrhs=nrhs, restart=2)
+    ie.ie_set_contrast(ctx, torch.from_numpy(cfg.sigma()).cuda())
+    ie.ie_set_source(ctx, np.array([s for s, _ in cfg.sources]), np.array([m for _, m in cfg.sources]))
+    nx, ny, nz = cfg.n
+    x = torch.empty((nrhs, 3, nz, ny, nx), dtype=torch.complex128, device="cuda")
+    ie.ie_get_incident(ctx, x)
+    y = torch.empty_like(x)
+    for _ in range(3):
+        ie.ie_apply_operator(ctx, x, y)
+    torch.cuda.synchronize()
+    ie.ie_profile(ctx, True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        ie.ie_apply_operator(ctx, x, y)
+    e1.record()
+    torch.cuda.synchronize()
+    prof = ie.ie_profile_read(ctx)
+    ie.ie_profile(ctx, False)
+    ms = e0.elapsed_time(e1) / steps
+    kc = prof["K-C z-convolution"]
+    kc_ms = kc[0] / max(1, kc[1])
+    R = 3 * nz
+    table = (nx + 1) * (ny + 1) * R * R * 16
+    x2 = 2 * nrhs * 12 * nx * ny * nz * 16
+    flops = 8 * R * R * 4 * nx * ny * nrhs
+    return {"workload": f"{name} grid, degenerate table (format 2), {nrhs} RHS", "ms_per_apply": round(ms, 4),
+            "kernels_ms": {k: round(v[0] / max(1, v[1]), 4) for k, v in prof.items()},
+            "k_c_prime": {"ms": round(kc_ms, 4), "alg_bytes": table + x2, "gbs": round((table + x2) / kc_ms / 1e6, 1),
+                          "fp64_tflops": round(flops / kc_ms / 1e9, 2), "pipe": "DMMA m8n8k4 f64 (tensor cores)"}}
+
+
 def cufft_reference(ctx, cfg, sigma, x, reps=5):
     """The same operator through torch.fft (cuFFT) + einsum on the full padded grid: a timing
     reference point only.  Uses the library's packed Green spectrum,
@@ -303,6 +345,7 @@ def run_ours(args, cfg, sigma, rank, ws, local):
            "d2h_bytes_per_step": int(yh.numel() * yh.element_size())}
 
     cufft = None if args.no_cufft else cufft_reference(ctx, cfg, sigma, x)
+    layered = None if args.no_layered else layered_leg()
 
     # --- forward solve seconds per tool position (full-domain GMRES vs DD schemes)
     dd = None
@@ -333,6 +376,7 @@ def run_ours(args, cfg, sigma, rank, ws, local):
                        "status": ie.STATUS.get(st["status"], st["status"])}
     return dict(value=value, per_step=per_step, launches=launches, clk=clk.summary(), peak=peak,
                 peak_src=peak_src, dom=dom, achieved=achieved, kernels=kernels, e2e=e2e, dd=dd, bm=bm, cufft=cufft,
+                layered=layered,
                 traffic=args.traffic)
 
 
@@ -347,6 +391,7 @@ def main():
     ap.add_argument("--dd-reps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-cufft", action="store_true")
+    ap.add_argument("--no-layered", action="store_true")
     ap.add_argument("--traffic", type=float, default=None, help="ncu dram bytes per launch of the dominant kernel")
     args = ap.parse_args()
     assert args.warmup >= 3 or args.impl == "reference" or args.warmup >= 0
@@ -383,7 +428,7 @@ def main():
                          "kernel": r["dom"], "peak_source": r["peak_src"]},
             "kernels": r["kernels"],
             "e2e": r["e2e"], "gpu_launches": r["launches"], "clocks": r["clk"],
-            "cpu_baseline": cpu, "cufft_reference": r["cufft"], "dd": r["dd"]}
+            "cpu_baseline": cpu, "cufft_reference": r["cufft"], "layered": r["layered"], "dd": r["dd"]}
     print(json.dumps(line))
 
 
