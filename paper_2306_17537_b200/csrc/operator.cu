@@ -10,15 +10,11 @@
 // The 1/(8 nx ny nz) normalisation is folded into the packed spectrum (green.cu).
 // See DESIGN.md §Kernels for the traffic model (1344 N + 96 (nx+1)(ny+1)(nz+1) bytes).
 #include <math.h>
-#include <stdlib.h>
 
 #include <unordered_map>
 #include <vector>
 
 #include "bulk_copy.cuh"
-#ifndef IE_KC_MERGE
-#define IE_KC_MERGE 0
-#endif
 #include "fft_core.cuh"
 #include "ie_internal.h"
 
@@ -255,7 +251,7 @@ __device__ __forceinline__ double2 cdot3(double2 g0, double2 j0, double2 g1, dou
 }
 
 template <int L, int W>
-__global__ void __launch_bounds__(W * L / 16, (W * L / 16 > 128) ? 1 : 2) k_zconv16(const __grid_constant__ ApplyParams p) {
+__global__ void __launch_bounds__(128, 2) k_zconv16(const __grid_constant__ ApplyParams p) {
   constexpr int T = L / 16, R1 = L / 16, U = 16 / R1, NZ = L / 2;
   static_assert(L == 64 || L == 128 || L == 256, "radix-16 z-pass: L in {64,128,256}");
   extern __shared__ __align__(16) double2 sm[];
@@ -299,14 +295,13 @@ __global__ void __launch_bounds__(W * L / 16, (W * L / 16 > 128) ? 1 : 2) k_zcon
 
   // L = 256 (U = 1): forward stage-1 twiddles w^(r t) and inverse ones conj(w^(r t)) are the
   // same 15 values for every component -- keep them in registers
-  constexpr bool kTwr = (L == 256) && !IE_KC_MERGE;
-  double2 twr[kTwr ? 16 : 1];
-  if constexpr (kTwr) {
+  double2 twr[L == 256 ? 16 : 1];
+  if constexpr (L == 256) {
 #pragma unroll
     for (int r = 1; r < 16; ++r) twr[r] = twl[r * t];
   }
   auto tw = [&](int r, int j) -> double2 {
-    if constexpr (kTwr) return twr[r];
+    if constexpr (L == 256) return twr[r];
     else return twl[r * j];
   };
 
@@ -368,51 +363,12 @@ __global__ void __launch_bounds__(W * L / 16, (W * L / 16 > 128) ? 1 : 2) k_zcon
     }
   };
 
-#if IE_KC_MERGE
-  // all three components in one pass: 3 independent butterfly chains per thread (ILP) and
-  // 2 barriers instead of 6
-  double2 Ga[B][6];
-  {
-    double2 v[3][16];
-#pragma unroll
-    for (int l = 0; l < 3; ++l)
-#pragma unroll
-      for (int r = 0; r < 8; ++r) v[l][r] = sm[(l * L + t + r * T) * W + c];
-#pragma unroll
-    for (int l = 0; l < 3; ++l) dft16<-1, true>(v[l]);
-    __syncthreads();
-#pragma unroll
-    for (int l = 0; l < 3; ++l)
-#pragma unroll
-      for (int r = 0; r < 16; ++r) sm[(l * L + t * 16 + r) * W + c] = v[l][r];
-    __syncthreads();
-    load_batch(Ga, 0);
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int j = t + u * T;
-#pragma unroll
-      for (int l = 0; l < 3; ++l) {
-#pragma unroll
-        for (int r = 0; r < R1; ++r) {
-          double2 x = sm[(l * L + j + r * 16) * W + c];
-          if (r > 0) x = cmul(x, twl[r * j]);
-          v[l][u * R1 + r] = x;
-        }
-        dftR<R1, -1>(&v[l][u * R1]);
-#pragma unroll
-        for (int r = 0; r < R1; ++r) sm[(l * L + j + r * 16) * W + c] = v[l][u * R1 + r];
-      }
-    }
-  }
-  __syncthreads();
-#else
   forward(0);
   forward(1);
   double2 Ga[B][6];
   load_batch(Ga, 0);  // in flight during the last forward FFT
   forward(2);
   __syncthreads();
-#endif
   if constexpr (2 * B == NQ) {
     double2 Gb[B][6];
     load_batch(Gb, B);
@@ -430,45 +386,6 @@ __global__ void __launch_bounds__(W * L / 16, (W * L / 16 > 128) ? 1 : 2) k_zcon
   __syncthreads();
 
   // ---- inverse z-FFTs (radix R1 then 16), crop to z < nz, store
-#if IE_KC_MERGE
-  {
-    double2 v[3][16];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int j = t + u * T;
-#pragma unroll
-      for (int l = 0; l < 3; ++l) {
-#pragma unroll
-        for (int r = 0; r < R1; ++r) v[l][u * R1 + r] = sm[(l * L + j + r * 16) * W + c];
-        dftR<R1, +1>(&v[l][u * R1]);
-      }
-    }
-    __syncthreads();
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int j = t + u * T;
-#pragma unroll
-      for (int l = 0; l < 3; ++l)
-#pragma unroll
-        for (int r = 0; r < R1; ++r) sm[(l * L + j * R1 + r) * W + c] = v[l][u * R1 + r];
-    }
-    __syncthreads();
-#pragma unroll
-    for (int l = 0; l < 3; ++l) {
-#pragma unroll
-      for (int r = 0; r < 16; ++r) {
-        double2 x = sm[(l * L + t + r * T) * W + c];
-        if (r > 0) x = cmulc(x, twl[r * t]);
-        v[l][r] = x;
-      }
-      dft16<+1, false, true>(v[l]);
-      double2* dst = tile + l * cs + c;
-#pragma unroll
-      for (int r = 0; r < 8; ++r) dst[(long long)(t + r * T) * zs] = v[l][r];
-    }
-  }
-  if (false)
-#endif
 #pragma unroll 1
   for (int l = 0; l < 3; ++l) {
     double2* S = sm + l * L * W;
@@ -734,7 +651,7 @@ static cudaError_t go_zconv16_w(const ApplyParams& p, cudaStream_t s) {
 }
 static cudaError_t go_zconv16(const ApplyParams& p, cudaStream_t s, int W) {
   const int L = 2 * p.nz;
-  if (L == 256) return getenv("IE_KC_W16") ? go_zconv16_w<256, 16>(p, s) : go_zconv16_w<256, 8>(p, s);
+  if (L == 256) return go_zconv16_w<256, 8>(p, s);
   if (L == 128) return W == 16 ? go_zconv16_w<128, 16>(p, s) : go_zconv16_w<128, 8>(p, s);
   if (L == 64)
     return W == 32 ? go_zconv16_w<64, 32>(p, s) : (W == 16 ? go_zconv16_w<64, 16>(p, s) : go_zconv16_w<64, 8>(p, s));
