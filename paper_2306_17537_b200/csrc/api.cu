@@ -4,6 +4,7 @@
 
 #include <algorithm>
 #include <complex>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <string>
@@ -169,6 +170,7 @@ ie_status ie_create(const ie_grid* g, const ie_background* bg, double freq_hz, v
   c->freq = freq_hz;
   c->omega = 2 * kPi * freq_hz;
   c->stream = (cudaStream_t)stream;
+  if (const char* sl = getenv("IE_SLABS")) c->slabs = sl[0] == '1';  // opt-in slab pipeline
   // k0 = sqrt(i omega mu0 sigma0), Re, Im > 0 (Eq. 7)
   c->k0 = std::sqrt(cplx(0.0, c->omega * kMu0 * c->sigma_b));
   // self term K(0) = (1/sigma0)[(2/3)(1 - i k0 a) e^{i k0 a} - 1]  (reading R3)
@@ -213,6 +215,11 @@ ie_status ie_destroy(ie_ctx* c) {
   cudaFree(c->d_red);
   if (c->h_red) cudaFreeHost(c->h_red);
   for (auto ev : c->ev_pool) cudaEventDestroy(ev);
+  if (c->aux_ready) {
+    for (auto st : c->aux) cudaStreamDestroy(st);
+    for (auto ev : c->aux_ev)
+      if (ev) cudaEventDestroy(ev);
+  }
   delete c;
   return IE_OK;
 }
@@ -637,13 +644,16 @@ ie_status ie_profile_read(ie_ctx* c, double* ms, int32_t* counts) {
     ms[k] = 0;
     counts[k] = 0;
   }
-  for (auto& mk : c->ev_marks)
-    for (int k = 0; k < 5; ++k) {
-      float t = 0;
-      IE_CUDA(c, cudaEventElapsedTime(&t, c->ev_pool[mk.second + k], c->ev_pool[mk.second + k + 1]));
-      ms[k] += t;
-      counts[k] += 1;
-    }
+  // per kernel: summed device time of its passes; counts = number of operator applications
+  // (a slab-pipelined application runs a kernel once per slab: those passes add to one count)
+  int applies = 0;
+  for (auto& mk : c->ev_marks) {
+    float t = 0;
+    IE_CUDA(c, cudaEventElapsedTime(&t, c->ev_pool[mk.ev0], c->ev_pool[mk.ev1]));
+    ms[mk.kernel] += t;
+    if (mk.kernel == 0) ++applies;
+  }
+  for (int k = 0; k < 5; ++k) counts[k] = applies;
   return IE_OK;
 }
 

@@ -38,7 +38,8 @@ struct ApplyParams {
   long long ds_cs, ds_zs, ds_ys;  // dsigma strides (doubles): component, z, y (x stride 1)
   const double2* ghat;            // packed spectrum [6][nz+1][ny+1][nx+1]
   double2* X1;                    // [item][3][nz][ny][2nx]
-  double2* X2;                    // [item][3][nz][2ny][2nx]
+  double2* X2;                    // [item][3][nz][2ny][x2w]
+  int x2w, k0x;                   // X2 row width and first kx it holds: (2nx, 0), or a slab
   double alpha, beta;
   int accumulate;
   const double2* tw_x;   // twiddles, L = 2nx, forward radix order
@@ -106,8 +107,16 @@ struct ie_ctx {
   // per-kernel profiling of the operator (ie_profile): events[i] brackets kernel kind[i]
   bool profiling = false;
   std::vector<cudaEvent_t> ev_pool;
-  std::vector<std::pair<int, int>> ev_marks;  // (kernel id, index of the start event)
+  struct Mark {
+    int kernel, ev0, ev1;  // kernel id 0..4 and the events bracketing one pass of it
+  };
+  std::vector<Mark> ev_marks;
   size_t ev_used = 0;
+  // L2-resident slab pipeline of the y/z passes (operator.cu): three streams, ring events
+  bool slabs = false;
+  bool aux_ready = false;
+  cudaStream_t aux[3] = {};
+  cudaEvent_t aux_ev[16] = {};
 };
 
 namespace ie {

@@ -11,6 +11,7 @@
 // See DESIGN.md §Kernels for the traffic model (1344 N + 96 (nx+1)(ny+1)(nz+1) bytes).
 #include <math.h>
 
+#include <algorithm>
 #include <unordered_map>
 #include <vector>
 
@@ -47,14 +48,16 @@ __global__ void __launch_bounds__(128, 4) k_xfwd(const __grid_constant__ ApplyPa
   const double* srow = it.dsig + zz * p.ds_zs + yy * p.ds_ys;
   const double xs = it.xscale;
 
-  double2 v[3][V];
+  // J for the thread's (non-zero) first-stage inputs, then one line FFT per component (a
+  // thread holds 3 x V/2 values of J plus the V values of the line in flight)
+  double2 J[3][V / 2];
 #pragma unroll
   for (int u = 0; u < V / R0; ++u)
 #pragma unroll
-    for (int r = 0; r < R0; ++r) {
+    for (int r = 0; r < R0 / 2; ++r) {  // r >= R0/2 <=> x >= nx: zero padding
       const int x = t + u * T + r * (L / R0);
       double2 J0 = czero(), J1 = czero(), J2 = czero();
-      if (r < R0 / 2 && valid && x >= it.sx0 && x < it.sx1) {  // r >= R0/2 <=> x >= nx: zero padding
+      if (valid && x >= it.sx0 && x < it.sx1) {
         const double2 e0 = cscale(ld2(xrow + x), xs);
         const double2 e1 = cscale(ld2(xrow + sN + x), xs);
         const double2 e2 = cscale(ld2(xrow + 2 * sN + x), xs);
@@ -65,21 +68,27 @@ __global__ void __launch_bounds__(128, 4) k_xfwd(const __grid_constant__ ApplyPa
         J1 = make_double2(sxy * e0.x + syy * e1.x + syz * e2.x, sxy * e0.y + syy * e1.y + syz * e2.y);
         J2 = make_double2(sxz * e0.x + syz * e1.x + szz * e2.x, sxz * e0.y + syz * e1.y + szz * e2.y);
       }
-      v[0][u * R0 + r] = J0;
-      v[1][u * R0 + r] = J1;
-      v[2][u * R0 + r] = J2;
+      J[0][u * (R0 / 2) + r] = J0;
+      J[1][u * (R0 / 2) + r] = J1;
+      J[2][u * (R0 / 2) + r] = J2;
     }
   const int region = padded(L);
-  auto idx = [&](int l) { return SIdx{(lr * 3 + l) * region, 1, 0}; };
-  fft_run<L, false, -1, 3>(v, sm, idx, t, p.tw_x, false);
-  if (!valid) return;
+  auto idx = [&](int) { return SIdx{lr * region, 1, 0}; };
 #pragma unroll
   for (int l = 0; l < 3; ++l) {
-    double2* out = p.X1 + ((((long long)blockIdx.y * 3 + l) * p.nz + zz) * p.ny + yy) * L;
+    double2 v[1][V];
 #pragma unroll
-    for (int u = 0; u < V / RL; ++u)
+    for (int u = 0; u < V / R0; ++u)
 #pragma unroll
-      for (int r = 0; r < RL; ++r) out[t + u * T + r * (L / RL)] = v[l][u * RL + r];
+      for (int r = 0; r < R0; ++r) v[0][u * R0 + r] = r < R0 / 2 ? J[l][u * (R0 / 2) + r] : czero();
+    fft_run<L, false, -1, 1>(v, sm, idx, t, p.tw_x, l > 0);
+    if (valid) {
+      double2* out = p.X1 + ((((long long)blockIdx.y * 3 + l) * p.nz + zz) * p.ny + yy) * L;
+#pragma unroll
+      for (int u = 0; u < V / RL; ++u)
+#pragma unroll
+        for (int r = 0; r < RL; ++r) out[t + u * T + r * (L / RL)] = v[0][u * RL + r];
+    }
   }
 }
 
@@ -93,8 +102,8 @@ __global__ void __launch_bounds__(512) k_yfwd(const __grid_constant__ ApplyParam
   const int c = threadIdx.x % W, t = threadIdx.x / W;
   const int item = blockIdx.z / 3, q = blockIdx.z % 3;
   const ApplyItem& it = p.items[item];
-  const int Lx = 2 * p.nx;
-  const int kx = blockIdx.x * W + c;
+  const int Lx = 2 * p.nx, Xw = p.x2w;  // X2 row width: 2nx, or the slab width (slab pipeline)
+  const int kx = p.k0x + blockIdx.x * W + c;
   const int z = it.sz0 + blockIdx.y;
   const double2* src = p.X1 + (((long long)item * 3 + q) * p.nz + z) * p.ny * Lx + kx;
   double2 v[1][V];
@@ -107,11 +116,11 @@ __global__ void __launch_bounds__(512) k_yfwd(const __grid_constant__ ApplyParam
     }
   auto idx = [&](int) { return SIdx{0, W, c}; };
   fft_run<L, false, -1, 1>(v, sm, idx, t, p.tw_y, false);
-  double2* dst = p.X2 + (((long long)item * 3 + q) * p.nz + z) * (long long)L * Lx + kx;
+  double2* dst = p.X2 + (((long long)item * 3 + q) * p.nz + z) * (long long)L * Xw + (kx - p.k0x);
 #pragma unroll
   for (int u = 0; u < V / RL; ++u)
 #pragma unroll
-    for (int r = 0; r < RL; ++r) dst[(long long)(t + u * T + r * (L / RL)) * Lx] = v[0][u * RL + r];
+    for (int r = 0; r < RL; ++r) dst[(long long)(t + u * T + r * (L / RL)) * Xw] = v[0][u * RL + r];
 }
 
 // =====================================================================  K-C
@@ -258,12 +267,12 @@ __global__ void __launch_bounds__(128, 2) k_zconv16(const __grid_constant__ Appl
   double2* twl = sm + 3 * L * W;  // exp(-2 pi i m / L), m < L
   const int c = threadIdx.x % W, t = threadIdx.x / W;
   const ApplyItem& it = p.items[blockIdx.z];
-  const int nx = p.nx, ny = p.ny, Lx = 2 * nx, Ly = 2 * ny;
-  const int kx0 = blockIdx.x * W, kx = kx0 + c;
+  const int nx = p.nx, ny = p.ny, Lx = 2 * nx, Ly = 2 * ny, Xw = p.x2w;
+  const int kx0 = p.k0x + blockIdx.x * W, kx = kx0 + c;
   const int by = blockIdx.y;  // mirror pairs (ky, 2ny-ky) adjacent in launch order (L2 reuse of G)
   const int ky = (by == 0) ? 0 : (by == 1 ? ny : ((by & 1) ? Ly - (by >> 1) : (by >> 1)));
-  const long long cs = (long long)NZ * Ly * Lx, zs = (long long)Ly * Lx;
-  double2* tile = p.X2 + (long long)blockIdx.z * 3 * cs + (long long)ky * Lx + kx0;
+  const long long cs = (long long)NZ * Ly * Xw, zs = (long long)Ly * Xw;
+  double2* tile = p.X2 + (long long)blockIdx.z * 3 * cs + (long long)ky * Xw + (kx0 - p.k0x);
   const long long gcs = (long long)(NZ + 1) * (ny + 1) * (nx + 1);
   const long long gzs = (long long)(ny + 1) * (nx + 1);
   const int ix = kx <= nx ? kx : Lx - kx;
@@ -427,15 +436,15 @@ __global__ void __launch_bounds__(512) k_yinv(const __grid_constant__ ApplyParam
   const int W = blockDim.x / T;
   const int c = threadIdx.x % W, t = threadIdx.x / W;
   const int item = blockIdx.z / 3, q = blockIdx.z % 3;
-  const int Lx = 2 * p.nx;
-  const int kx = blockIdx.x * W + c;
+  const int Lx = 2 * p.nx, Xw = p.x2w;
+  const int kx = p.k0x + blockIdx.x * W + c;
   const int z = blockIdx.y;
-  const double2* src = p.X2 + (((long long)item * 3 + q) * p.nz + z) * (long long)L * Lx + kx;
+  const double2* src = p.X2 + (((long long)item * 3 + q) * p.nz + z) * (long long)L * Xw + (kx - p.k0x);
   double2 v[1][V];
 #pragma unroll
   for (int u = 0; u < V / R0; ++u)
 #pragma unroll
-    for (int r = 0; r < R0; ++r) v[0][u * R0 + r] = src[(long long)(t + u * T + r * (L / R0)) * Lx];
+    for (int r = 0; r < R0; ++r) v[0][u * R0 + r] = src[(long long)(t + u * T + r * (L / R0)) * Xw];
   auto idx = [&](int) { return SIdx{0, W, c}; };
   fft_run<L, false, +1, 1>(v, sm, idx, t, p.tw_y, false);
   double2* dst = p.X1 + (((long long)item * 3 + q) * p.nz + z) * p.ny * Lx + kx;
@@ -446,12 +455,16 @@ __global__ void __launch_bounds__(512) k_yinv(const __grid_constant__ ApplyParam
 }
 
 // =====================================================================  K-E
+// One component per CTA row group (blockIdx.y = item*3 + component): the inverse x-FFT and
+// the identity update never mix components, so a thread holds one line (8 values) and the
+// kernel runs at high occupancy.
 template <int L>
-__global__ void __launch_bounds__(256) k_xinv(const __grid_constant__ ApplyParams p) {
+__global__ void __launch_bounds__(128) k_xinv(const __grid_constant__ ApplyParams p) {
   using P = FftPlan<L>;
   constexpr int T = P::T, V = P::V, R0 = P::radix(0, false), RL = P::radix(P::NST - 1, false);
   extern __shared__ double2 sm[];
-  const ApplyItem& it = p.items[blockIdx.y];
+  const int item = blockIdx.y / 3, l = blockIdx.y % 3;
+  const ApplyItem& it = p.items[item];
   const int rows_cta = blockDim.x / T;
   const int lr = threadIdx.x / T, t = threadIdx.x % T;
   const int nx = p.nx, ny = p.ny, nz = p.nz;
@@ -459,40 +472,36 @@ __global__ void __launch_bounds__(256) k_xinv(const __grid_constant__ ApplyParam
   const bool valid = row < ny * nz;
   const int yy = valid ? row % ny : 0, zz = valid ? row / ny : 0;
   const long long N = (long long)nx * ny * nz;
-  double2 v[3][V];
-#pragma unroll
-  for (int l = 0; l < 3; ++l) {
-    const double2* src = p.X1 + ((((long long)blockIdx.y * 3 + l) * nz + zz) * ny + yy) * L;
+  double2 v[1][V];
+  {
+    const double2* src = p.X1 + ((((long long)item * 3 + l) * nz + zz) * ny + yy) * L;
 #pragma unroll
     for (int u = 0; u < V / R0; ++u)
 #pragma unroll
-      for (int r = 0; r < R0; ++r) v[l][u * R0 + r] = valid ? src[t + u * T + r * (L / R0)] : czero();
+      for (int r = 0; r < R0; ++r) v[0][u * R0 + r] = valid ? src[t + u * T + r * (L / R0)] : czero();
   }
   const int region = padded(L);
-  auto idx = [&](int l) { return SIdx{(lr * 3 + l) * region, 1, 0}; };
-  fft_run<L, false, +1, 3>(v, sm, idx, t, p.tw_x, false);
+  auto idx = [&](int) { return SIdx{lr * region, 1, 0}; };
+  fft_run<L, false, +1, 1>(v, sm, idx, t, p.tw_x, false);
   if (!valid) return;
   const long long off = ((long long)zz * ny + yy) * nx;
   const double a = p.alpha * it.xscale, b = p.beta;
+  double2* yrow = it.y + l * N + off;
+  const double2* xrow = it.x + l * N + off;
 #pragma unroll
-  for (int l = 0; l < 3; ++l) {
-    double2* yrow = it.y + l * N + off;
-    const double2* xrow = it.x + l * N + off;
+  for (int u = 0; u < V / RL; ++u)
 #pragma unroll
-    for (int u = 0; u < V / RL; ++u)
-#pragma unroll
-      for (int r = 0; r < RL / 2; ++r) {  // x >= nx discarded (crop)
-        const int x = t + u * T + r * (L / RL);
-        double2 o = cscale(v[l][u * RL + r], b);
-        if (a != 0.0) {
-          const double2 xi = ld2(xrow + x);
-          o.x = fma(a, xi.x, o.x);
-          o.y = fma(a, xi.y, o.y);
-        }
-        if (p.accumulate) o = cadd(o, yrow[x]);
-        yrow[x] = o;
+    for (int r = 0; r < RL / 2; ++r) {  // x >= nx discarded (crop)
+      const int x = t + u * T + r * (L / RL);
+      double2 o = cscale(v[0][u * RL + r], b);
+      if (a != 0.0) {
+        const double2 xi = ld2(xrow + x);
+        o.x = fma(a, xi.x, o.x);
+        o.y = fma(a, xi.y, o.y);
       }
-  }
+      if (p.accumulate) o = cadd(o, yrow[x]);
+      yrow[x] = o;
+    }
 }
 
 // =====================================================================  host side
@@ -609,7 +618,7 @@ static int z_width(int L, int T, int Lx) {
 template <int L>
 static cudaError_t go_xfwd(const ApplyParams& p, cudaStream_t s, int max_rows) {
   const int T = FftPlan<L>::T, rows = rows_per_cta(T);
-  const size_t smem = (size_t)rows * 3 * padded(L) * sizeof(double2);
+  const size_t smem = (size_t)rows * padded(L) * sizeof(double2);
   cudaError_t e = prep((const void*)k_xfwd<L>, smem);
   if (e) return e;
   k_xfwd<L><<<dim3((max_rows + rows - 1) / rows, p.n_items), rows * T, smem, s>>>(p);
@@ -621,7 +630,7 @@ static cudaError_t go_yfwd(const ApplyParams& p, cudaStream_t s, int max_planes)
   const size_t smem = (size_t)padded(L * W) * sizeof(double2);
   cudaError_t e = prep((const void*)k_yfwd<L>, smem);
   if (e) return e;
-  k_yfwd<L><<<dim3(2 * p.nx / W, max_planes, 3 * p.n_items), W * T, smem, s>>>(p);
+  k_yfwd<L><<<dim3(p.x2w / W, max_planes, 3 * p.n_items), W * T, smem, s>>>(p);
   return cudaGetLastError();
 }
 template <int L>
@@ -646,7 +655,7 @@ static cudaError_t go_zconv16_w(const ApplyParams& p, cudaStream_t s) {
   const size_t smem = (size_t)(3 * L * W + L) * sizeof(double2);
   cudaError_t e = prep((const void*)k_zconv16<L, W>, smem);
   if (e) return e;
-  k_zconv16<L, W><<<dim3(2 * p.nx / W, 2 * p.ny, p.n_items), W * (L / 16), smem, s>>>(p);
+  k_zconv16<L, W><<<dim3(p.x2w / W, 2 * p.ny, p.n_items), W * (L / 16), smem, s>>>(p);
   return cudaGetLastError();
 }
 static cudaError_t go_zconv16(const ApplyParams& p, cudaStream_t s, int W) {
@@ -663,16 +672,16 @@ static cudaError_t go_yinv(const ApplyParams& p, cudaStream_t s) {
   const size_t smem = (size_t)padded(L * W) * sizeof(double2);
   cudaError_t e = prep((const void*)k_yinv<L>, smem);
   if (e) return e;
-  k_yinv<L><<<dim3(2 * p.nx / W, p.nz, 3 * p.n_items), W * T, smem, s>>>(p);
+  k_yinv<L><<<dim3(p.x2w / W, p.nz, 3 * p.n_items), W * T, smem, s>>>(p);
   return cudaGetLastError();
 }
 template <int L>
 static cudaError_t go_xinv(const ApplyParams& p, cudaStream_t s) {
   const int T = FftPlan<L>::T, rows = rows_per_cta(T);
-  const size_t smem = (size_t)rows * 3 * padded(L) * sizeof(double2);
+  const size_t smem = (size_t)rows * padded(L) * sizeof(double2);
   cudaError_t e = prep((const void*)k_xinv<L>, smem);
   if (e) return e;
-  k_xinv<L><<<dim3((p.ny * p.nz + rows - 1) / rows, p.n_items), rows * T, smem, s>>>(p);
+  k_xinv<L><<<dim3((p.ny * p.nz + rows - 1) / rows, 3 * p.n_items), rows * T, smem, s>>>(p);
   return cudaGetLastError();
 }
 
@@ -682,26 +691,57 @@ template <int L> static void wrap_zconv(cudaError_t* e, const ApplyParams& p, cu
 template <int L> static void wrap_yinv(cudaError_t* e, const ApplyParams& p, cudaStream_t s) { *e = go_yinv<L>(p, s); }
 template <int L> static void wrap_xinv(cudaError_t* e, const ApplyParams& p, cudaStream_t s) { *e = go_xinv<L>(p, s); }
 
-static cudaError_t run_apply(const ApplyParams& p, cudaStream_t s, cudaEvent_t* ev) {
-  cudaError_t e = cudaSuccess;
-  int max_rows = 0, max_planes = 0;
+// Profiling: each kernel pass is bracketed by two events on the stream it runs on; a mark
+// (kernel id, start event, end event) per bracket.
+struct Prof {
+  ie_ctx* c;
+  cudaError_t take(int n, int* first) {
+    if (!c->profiling) return cudaSuccess;
+    while (c->ev_pool.size() < c->ev_used + n) {
+      cudaEvent_t x;
+      cudaError_t e = cudaEventCreate(&x);
+      if (e) return e;
+      c->ev_pool.push_back(x);
+    }
+    *first = (int)c->ev_used;
+    c->ev_used += n;
+    return cudaSuccess;
+  }
+  void rec(int idx, cudaStream_t s) {
+    if (c->profiling) cudaEventRecord(c->ev_pool[idx], s);
+  }
+  void mark(int kernel, int i0, int i1) {
+    if (c->profiling) c->ev_marks.push_back({kernel, i0, i1});
+  }
+};
+
+static void source_extent(const ApplyParams& p, int* max_rows, int* max_planes) {
+  *max_rows = 0;
+  *max_planes = 0;
   for (int i = 0; i < p.n_items; ++i) {
     const ApplyItem& it = p.items[i];
     const int rows = (it.sy1 - it.sy0) * (it.sz1 - it.sz0);
-    if (rows > max_rows) max_rows = rows;
-    if (it.sz1 - it.sz0 > max_planes) max_planes = it.sz1 - it.sz0;
+    if (rows > *max_rows) *max_rows = rows;
+    if (it.sz1 - it.sz0 > *max_planes) *max_planes = it.sz1 - it.sz0;
   }
-  auto mark = [&](int k) {
-    if (ev) cudaEventRecord(ev[k], s);
-  };
+}
+
+// The five passes in one stream, X2 holding the whole padded grid.
+static cudaError_t run_apply(ie_ctx* c, const ApplyParams& p, cudaStream_t s) {
+  cudaError_t e = cudaSuccess;
+  int max_rows, max_planes;
+  source_extent(p, &max_rows, &max_planes);
+  Prof pr{c};
+  int ev = 0;
+  if ((e = pr.take(6, &ev))) return e;
   // items of one launch share the source y/z range (K-A rows, K-B planes)
-  mark(0);
+  pr.rec(ev + 0, s);
   IE_DISPATCH_L(2 * p.nx, wrap_xfwd, &e, p, s, max_rows);
   if (e) return e;
-  mark(1);
+  pr.rec(ev + 1, s);
   IE_DISPATCH_L(2 * p.ny, wrap_yfwd, &e, p, s, max_planes);
   if (e) return e;
-  mark(2);
+  pr.rec(ev + 2, s);
   if (p.mhat) {  // layered background: z-z' contraction per horizontal wavenumber (layered.cu)
     e = launch_zlayer(p, s);
   } else if (const int W16 = zconv16_width(2 * p.nz, 2 * p.nx)) {
@@ -710,12 +750,109 @@ static cudaError_t run_apply(const ApplyParams& p, cudaStream_t s, cudaEvent_t* 
     IE_DISPATCH_L(2 * p.nz, wrap_zconv, &e, p, s);
   }
   if (e) return e;
-  mark(3);
+  pr.rec(ev + 3, s);
   IE_DISPATCH_L(2 * p.ny, wrap_yinv, &e, p, s);
   if (e) return e;
-  mark(4);
+  pr.rec(ev + 4, s);
   IE_DISPATCH_L(2 * p.nx, wrap_xinv, &e, p, s);
-  mark(5);
+  pr.rec(ev + 5, s);
+  for (int k = 0; k < 5; ++k) pr.mark(k, ev + k, ev + k + 1);
+  c->launches += 5;
+  return e;
+}
+
+// ---------------------------------------------------------------- L2-resident slab pipeline
+// For grids whose padded intermediate X2 (192 N bytes per item) is far larger than L2, the
+// y-forward, z-convolution and y-inverse passes run slab by slab over S consecutive kx
+// columns, each slab's X2 ([item][3][nz][2ny][S]) in a ring of NR buffers small enough to stay
+// in the 126 MB L2: K-B(s) writes it, K-C(s) transforms it in place, K-D(s) reads it, and the
+// HBM never sees X2 (traffic per apply 576 N + |G| instead of 1344 N + |G| bytes).  The three
+// passes run on three streams ordered by events, so slab s+1's K-B overlaps slab s's K-C and
+// slab s-1's K-D.
+constexpr int kSlabRing = 3;
+constexpr size_t kSlabL2Budget = 80ull << 20;  // bytes of X2 ring kept in flight
+
+static int slab_width(const ApplyParams& p) {
+  if (p.mhat) return 0;
+  const int Lx = 2 * p.nx;
+  const int W16 = zconv16_width(2 * p.nz, Lx);
+  if (!W16) return 0;
+  const int Ty = (2 * p.ny) / std::min(8, 2 * p.ny);  // threads per y-line (FftPlan<2ny>::T)
+  const int Wy = y_width(Ty, Lx);                     // K-B / K-D tile width
+  const int S = std::max(W16, Wy);
+  if (S > Lx || Lx % S) return 0;
+  const size_t full = (size_t)p.n_items * 3 * p.nz * 2 * p.ny * Lx * sizeof(double2);
+  const size_t slab = (size_t)p.n_items * 3 * p.nz * 2 * p.ny * S * sizeof(double2);
+  if (full <= 2 * kSlabL2Budget || kSlabRing * slab > kSlabL2Budget) return 0;
+  return S;
+}
+
+static cudaError_t ensure_aux(ie_ctx* c) {
+  if (c->aux_ready) return cudaSuccess;
+  cudaError_t e;
+  for (int i = 0; i < 3; ++i)
+    if ((e = cudaStreamCreateWithFlags(&c->aux[i], cudaStreamNonBlocking))) return e;
+  for (int i = 0; i < 1 + 3 * kSlabRing; ++i)
+    if ((e = cudaEventCreateWithFlags(&c->aux_ev[i], cudaEventDisableTiming))) return e;
+  c->aux_ready = true;
+  return cudaSuccess;
+}
+
+static cudaError_t run_apply_slabs(ie_ctx* c, const ApplyParams& p, cudaStream_t s, int S) {
+  cudaError_t e = cudaSuccess;
+  if ((e = ensure_aux(c))) return e;
+  int max_rows, max_planes;
+  source_extent(p, &max_rows, &max_planes);
+  const int Lx = 2 * p.nx, nslab = Lx / S;
+  const long long slab_elems = (long long)p.n_items * 3 * p.nz * 2 * p.ny * S;
+  cudaEvent_t evA = c->aux_ev[0];
+  cudaEvent_t* evB = c->aux_ev + 1;
+  cudaEvent_t* evC = c->aux_ev + 1 + kSlabRing;
+  cudaEvent_t* evD = c->aux_ev + 1 + 2 * kSlabRing;
+  cudaStream_t sB = c->aux[0], sC = c->aux[1], sD = c->aux[2];
+  Prof pr{c};
+  int ev = 0;
+  if ((e = pr.take(4 + 6 * nslab, &ev))) return e;
+  pr.rec(ev + 0, s);
+  IE_DISPATCH_L(2 * p.nx, wrap_xfwd, &e, p, s, max_rows);
+  if (e) return e;
+  pr.rec(ev + 1, s);
+  pr.mark(0, ev + 0, ev + 1);
+  if ((e = cudaEventRecord(evA, s))) return e;
+  for (cudaStream_t x : {sB, sC, sD})
+    if ((e = cudaStreamWaitEvent(x, evA, 0))) return e;
+  for (int sl = 0; sl < nslab; ++sl) {
+    const int b = sl % kSlabRing;
+    ApplyParams q = p;
+    q.X2 = p.X2 + b * slab_elems;
+    q.x2w = S;
+    q.k0x = sl * S;
+    const int e0 = ev + 4 + 6 * sl;
+    if (sl >= kSlabRing && (e = cudaStreamWaitEvent(sB, evD[b], 0))) return e;  // buffer b free
+    pr.rec(e0 + 0, sB);
+    IE_DISPATCH_L(2 * p.ny, wrap_yfwd, &e, q, sB, max_planes);
+    if (e) return e;
+    pr.rec(e0 + 1, sB);
+    if ((e = cudaEventRecord(evB[b], sB)) || (e = cudaStreamWaitEvent(sC, evB[b], 0))) return e;
+    pr.rec(e0 + 2, sC);
+    if ((e = go_zconv16(q, sC, zconv16_width(2 * p.nz, Lx)))) return e;
+    pr.rec(e0 + 3, sC);
+    if ((e = cudaEventRecord(evC[b], sC)) || (e = cudaStreamWaitEvent(sD, evC[b], 0))) return e;
+    pr.rec(e0 + 4, sD);
+    IE_DISPATCH_L(2 * p.ny, wrap_yinv, &e, q, sD);
+    if (e) return e;
+    pr.rec(e0 + 5, sD);
+    if ((e = cudaEventRecord(evD[b], sD))) return e;
+    pr.mark(1, e0 + 0, e0 + 1);
+    pr.mark(2, e0 + 2, e0 + 3);
+    pr.mark(3, e0 + 4, e0 + 5);
+  }
+  if ((e = cudaStreamWaitEvent(s, evD[(nslab - 1) % kSlabRing], 0))) return e;
+  pr.rec(ev + 2, s);
+  IE_DISPATCH_L(2 * p.nx, wrap_xinv, &e, p, s);
+  pr.rec(ev + 3, s);
+  pr.mark(4, ev + 2, ev + 3);
+  c->launches += 2 + 3 * nslab;
   return e;
 }
 
@@ -731,19 +868,10 @@ ie_status launch_apply(ie_ctx* c, ApplyParams& p) {
   p.tw_z = c->tw.get(2 * p.nz, 0);
   p.tw_zr = c->tw.get(2 * p.nz, 1);
   p.pw_z = c->tw.powers(2 * p.nz);
-  cudaEvent_t* ev = nullptr;
-  if (c->profiling) {
-    while (c->ev_pool.size() < c->ev_used + 6) {
-      cudaEvent_t x;
-      IE_CUDA(c, cudaEventCreate(&x));
-      c->ev_pool.push_back(x);
-    }
-    ev = &c->ev_pool[c->ev_used];
-    c->ev_marks.push_back({0, (int)c->ev_used});
-    c->ev_used += 6;
-  }
-  cudaError_t e = run_apply(p, c->stream, ev);
-  c->launches += 5;
+  p.x2w = 2 * p.nx;
+  p.k0x = 0;
+  const int S = c->slabs ? slab_width(p) : 0;  // off unless IE_SLABS=1 (measured slower)
+  cudaError_t e = S ? run_apply_slabs(c, p, c->stream, S) : run_apply(c, p, c->stream);
   if (e != cudaSuccess) return cuda_fail(c, e, "operator kernels");
   return IE_OK;
 }
