@@ -18,7 +18,7 @@
 
 namespace ie {
 
-constexpr int kDotG = 16;  // basis vectors per pass over w
+constexpr int kDotG = 8;  // basis vectors per pass over w (one CTA group each)
 
 struct DotJob {
   const double2* w;
@@ -38,45 +38,60 @@ __device__ __forceinline__ double2 shfl_down2(double2 v, int d) {
   return make_double2(__shfl_down_sync(0xffffffffu, v.x, d), __shfl_down_sync(0xffffffffu, v.y, d));
 }
 
+// Dot products of w with G consecutive basis vectors (and ||w||^2 when the group reaches
+// row nv): blockIdx.y selects the group, blockIdx.z the job.  All G+1 loads of an element
+// are issued before the FMAs (uniform predicates, no divergence) so each thread keeps
+// (G+1) x 16 bytes in flight; two elements per thread per trip for more memory parallelism.
+template <int G>
 __global__ void __launch_bounds__(256) k_mdot(const DotJob* __restrict__ jobs, long long len, double2* __restrict__ part,
                                               int nblk) {
-  const DotJob jb = jobs[blockIdx.y];
-  __shared__ double2 red[8][kDotG];
+  const DotJob jb = jobs[blockIdx.z];
+  const int g0 = blockIdx.y * G;
+  if (g0 > jb.nv) return;
+  __shared__ double2 red[8][G];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  for (int j0 = 0; j0 <= jb.nv; j0 += kDotG) {
-    double2 acc[kDotG];
+  double2 acc[G];
 #pragma unroll
-    for (int g = 0; g < kDotG; ++g) acc[g] = czero();
-    for (long long i = blockIdx.x * 256LL + threadIdx.x; i < len; i += (long long)nblk * 256) {
-      const double2 w = jb.w[i];
+  for (int g = 0; g < G; ++g) acc[g] = czero();
+  const long long stride = (long long)nblk * 256;
+  for (long long i = blockIdx.x * 256LL + threadIdx.x; i < len; i += 2 * stride) {
+    const long long i2 = i + stride;
+    const bool ok2 = i2 < len;
+    double2 w[2], v[2][G];
+    w[0] = jb.w[i];
+    w[1] = ok2 ? jb.w[i2] : czero();
 #pragma unroll
-      for (int g = 0; g < kDotG; ++g) {
-        const int j = j0 + g;
-        if (j < jb.nv) {
-          const double2 v = jb.V[(long long)j * len + i];
-          acc[g].x = fma(v.x, w.x, fma(v.y, w.y, acc[g].x));  // conj(v) * w
-          acc[g].y = fma(v.x, w.y, fma(-v.y, w.x, acc[g].y));
-        } else if (j == jb.nv) {
-          acc[g].x = fma(w.x, w.x, fma(w.y, w.y, acc[g].x));
+    for (int g = 0; g < G; ++g) {
+      const bool on = g0 + g < jb.nv;
+      v[0][g] = on ? jb.V[(long long)(g0 + g) * len + i] : czero();
+      v[1][g] = (on && ok2) ? jb.V[(long long)(g0 + g) * len + i2] : czero();
+    }
+#pragma unroll
+    for (int e = 0; e < 2; ++e)
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        if (g0 + g < jb.nv) {
+          acc[g].x = fma(v[e][g].x, w[e].x, fma(v[e][g].y, w[e].y, acc[g].x));  // conj(v) * w
+          acc[g].y = fma(v[e][g].x, w[e].y, fma(-v[e][g].y, w[e].x, acc[g].y));
+        } else if (g0 + g == jb.nv) {
+          acc[g].x = fma(w[e].x, w[e].x, fma(w[e].y, w[e].y, acc[g].x));
         }
       }
-    }
+  }
 #pragma unroll
-    for (int g = 0; g < kDotG; ++g) {
+  for (int g = 0; g < G; ++g) {
 #pragma unroll
-      for (int d = 16; d > 0; d >>= 1) acc[g] = cadd(acc[g], shfl_down2(acc[g], d));
-    }
-    if (lane == 0)
+    for (int d = 16; d > 0; d >>= 1) acc[g] = cadd(acc[g], shfl_down2(acc[g], d));
+  }
+  if (lane == 0)
 #pragma unroll
-      for (int g = 0; g < kDotG; ++g) red[wid][g] = acc[g];
-    __syncthreads();
-    if (threadIdx.x < kDotG) {
-      const int j = j0 + threadIdx.x;
-      double2 s = czero();
-      for (int w8 = 0; w8 < 8; ++w8) s = cadd(s, red[w8][threadIdx.x]);
-      if (j <= jb.nv) part[(long long)(jb.row + j) * nblk + blockIdx.x] = s;
-    }
-    __syncthreads();
+    for (int g = 0; g < G; ++g) red[wid][g] = acc[g];
+  __syncthreads();
+  if (threadIdx.x < G) {
+    const int j = g0 + threadIdx.x;
+    double2 sum = czero();
+    for (int w8 = 0; w8 < 8; ++w8) sum = cadd(sum, red[w8][threadIdx.x]);
+    if (j <= jb.nv) part[(long long)(jb.row + j) * nblk + blockIdx.x] = sum;
   }
 }
 
@@ -247,7 +262,9 @@ ie_status gmres_batched(ie_ctx* c, Arena& ar, int nx, int ny, int nz, int k0, lo
       row += nv[i] + 1;
     }
     IE_CUDA(c, cudaMemcpyAsync(d_dot, hj, n * sizeof(DotJob), cudaMemcpyHostToDevice, c->stream));
-    k_mdot<<<dim3(nblk, n), 256, 0, c->stream>>>(d_dot, len, part, nblk);
+    int maxnv = 0;
+    for (int i = 0; i < n; ++i) maxnv = std::max(maxnv, nv[i]);
+    k_mdot<kDotG><<<dim3(nblk, maxnv / kDotG + 1, n), 256, 0, c->stream>>>(d_dot, len, part, nblk);
     IE_CHECK_LAUNCH(c, "k_mdot");
     k_reduce_rows<<<row, 128, 0, c->stream>>>(part, nblk, rows);
     IE_CHECK_LAUNCH(c, "k_reduce_rows");
