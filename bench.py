@@ -121,13 +121,21 @@ def dist_init():
 
 
 def max_over_ranks(v, ws):
+    """Slowest rank's value (device-timed milliseconds): the replica job's time."""
     if ws <= 1:
         return v
     import torch
     import torch.distributed as dist
-    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([v], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
+
+
+def replica_value(bytes_per_step, steps, t_ms_max, ws):
+    """Whole-job throughput of N independent replicas (SURVEY 8(e), weak scaling): all ranks'
+    algorithmic bytes over the max-over-ranks device time, GB/s."""
+    return ws * bytes_per_step * steps / (t_ms_max / 1e3) / 1e9
 
 
 def barrier(ws):
@@ -310,7 +318,7 @@ def run_ours(args, cfg, sigma, rank, ws, local):
     t_ms = max_over_ranks(t_ms, ws)
     per_step = t_ms / args.steps
     bm = b_model(nx, ny, nz)
-    value = ws * bm * args.steps / (t_ms / 1e3) / 1e9
+    value = replica_value(bm, args.steps, t_ms, ws)
     peak, peak_src = peaks()
 
     # roofline of the dominant kernel (largest share of the step)
