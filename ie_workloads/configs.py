@@ -10,7 +10,10 @@ DESIGN.md §Inputs; variants:
   c2mod     the c2 geometry with moderate contrast: sigma_h = sigma_b 10^U[-0.3,0.7],
             sigma_v/sigma_h ~ U[0.3,1] (oracle GMRES(30) reaches 1e-11 in 56 iterations)
   c3h, c4h  the c3 / c4 grids, contrast recipes and tools on a HOMOGENEOUS background
-            (sigma_b = 1 S/m, 400 kHz): the layered-table path (A3L) is not built yet.
+            (c3h: sigma_b = 1 S/m; c4h: sigma_b = 0.01 S/m, the middle layer that holds the
+            slab and the trajectory -- in a 1 S/m host the sigma_v = 0.005 slab is a 200x
+            resistive body and conventional-IE GMRES stagnates at 3e-4); the layered path
+            runs on the degenerate table (R19).
   *mini     the same recipe on an 8^3 grid so that dense LU gives exact truth.
 """
 
@@ -214,11 +217,12 @@ def make_config(name):
                       boxes=box_grid((8, 8, 8), (2, 2, 1)), restart=30, outer_tol=1e-9)
     if name == "c4h":
         st = c4_stations()
-        return Config(name, (128, 128, 64), 0.25, 1.0, 4e5, 4, _c4_sigma,
+        return Config(name, (128, 128, 64), 0.25, 0.01, 4e5, 4, _c4_sigma,
                       sources=[(st[31]["tx"], st[31]["moments"][i]) for i in range(3)],
                       receivers=list(st[31]["rx"]),
                       boxes=box_grid((128, 128, 64), (4, 2, 1)), restart=30, outer_tol=1e-6,
-                      note="homogeneous stand-in for the layered c4 (sigma_b = 1 S/m, 400 kHz)")
+                      note="homogeneous stand-in for the layered c4 at its middle-layer conductivity "
+                           "(sigma_b = 0.01 S/m, 400 kHz): the slab and the trajectory sit in that layer")
     if name == "c5":
         return Config(name, (256, 256, 128), 0.2, 0.5, 1e5, 5, _c5_sigma,
                       sources=[(np.zeros(3), zdip)],
