@@ -48,6 +48,16 @@ def kernel_bytes(nx, ny, nz):
             "K-E x-inverse+update": 96 * N + 48 * N + 48 * N}
 
 
+def ncu_traffic(workload, kernel):
+    """DRAM bytes per launch of `kernel` on `workload` from the committed ncu --set full capture
+    summary (profiles/ncu_traffic.json: dram__bytes_read.sum + dram__bytes_write.sum), or None."""
+    try:
+        t = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+        return t[workload][kernel]
+    except Exception:
+        return None
+
+
 def peaks():
     try:
         mp = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -473,6 +483,8 @@ def main():
             print(json.dumps(line))
         return
     r = run_ours(args, cfg, sigma, rank, ws, local)
+    if r["traffic"] is None:
+        r["traffic"] = ncu_traffic(cfg.name, r["dom"])
     if rank != 0:
         return
     cpu = None
