@@ -373,9 +373,9 @@ __global__ void __launch_bounds__(128, 2) k_zconv16(const __grid_constant__ Appl
   };
 
   forward(0);
-  forward(1);
   double2 Ga[B][6];
-  load_batch(Ga, 0);  // in flight during the last forward FFT
+  load_batch(Ga, 0);  // in flight during the last two forward FFTs
+  forward(1);
   forward(2);
   __syncthreads();
   if constexpr (2 * B == NQ) {
