@@ -47,3 +47,34 @@ def test_fullsize_operator_sampled_cells(name):
     ie.ie_apply_operator(ctx, z, v)
     lin = (2.0 + 1j) * y + v
     assert float(torch.linalg.vector_norm(w - lin) / torch.linalg.vector_norm(lin)) < 1e-13
+
+
+@pytest.mark.parametrize("name,scheme", [("c5", "full"), ("c5", "gauss_seidel"), ("c4h", "full")])
+def test_fullsize_solve_residual_at_sampled_cells(name, scheme):
+    """Full-size forward solves as bench.py runs them: the Eq. 9 residual E0 - (I - G dsigma) E
+    evaluated by the oracle's direct summation (one output cell at a time) at sampled cells is
+    at the solver tolerance, and the library's reported e is <= outer_tol."""
+    import torch
+    import paper_2306_17537_b200 as ie
+    cfg = make_config(name)
+    sigma = cfg.sigma()
+    ctx, _ = gpu_ctx(cfg, sigma=sigma, boxes=cfg.boxes, nrhs=len(cfg.sources), restart=cfg.restart)
+    nx, ny, nz = cfg.n
+    e = torch.empty((len(cfg.sources), 3, nz, ny, nx), dtype=torch.complex128, device="cuda")
+    tol = 1e-7
+    st = ie.ie_solve_dd(ctx, e, scheme, boxes=cfg.boxes, outer_tol=tol, restart=cfg.restart, max_sweeps=100,
+                        max_iters=3000)
+    assert st["e_final"] <= tol
+    e0 = torch.empty_like(e)
+    ie.ie_get_incident(ctx, e0)
+    E = e.cpu().numpy()[0]
+    E0 = e0.cpu().numpy()[0]
+    k0 = physics.wavenumber(cfg.sigma_b, cfg.freq)
+    ds = physics.contrast(sigma, cfg.sigma_b)
+    rng = np.random.default_rng(1)
+    cells = [(nx // 2, ny // 2, nz // 2)] + [tuple(int(v) for v in rng.integers(0, [nx, ny, nz])) for _ in range(2)]
+    AE = op.direct_rows(cfg.n, cfg.hvec, k0, cfg.sigma_b, ds, E, cells)
+    scale = np.linalg.norm(E0.ravel()) / np.sqrt(E0.size)  # rms of E0
+    for t, (cx, cy, cz) in enumerate(cells):
+        r = E0[:, cz, cy, cx] - AE[t]
+        assert np.abs(r).max() < 100 * tol * max(scale, np.abs(E0[:, cz, cy, cx]).max()), (cells[t], r)
