@@ -156,6 +156,10 @@ typedef struct {
   int32_t max_iters; /* cap on A v products */
   int32_t min_iters; /* >= 0 */
   double tol;        /* relative residual target, > 0 */
+  int32_t precond;   /* 0: the paper's conventional IE; 1: contraction-IE right preconditioner
+                        P = 2 sigma_b (sigma + sigma_b I)^-1 per cell (Hursan & Zhdanov; the paper's
+                        remedy for high contrast): GMRES on (I - G dsigma) P chi = E0,
+                        E = P chi -- same solution, same Eq. 9 residual */
 } ie_gmres_opts;
 typedef struct {
   int32_t iters, restarts, converged;

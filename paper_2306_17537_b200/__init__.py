@@ -57,7 +57,7 @@ class ie_box(ctypes.Structure):
 
 class ie_gmres_opts(ctypes.Structure):
     _fields_ = [("restart", ctypes.c_int32), ("max_iters", ctypes.c_int32), ("min_iters", ctypes.c_int32),
-                ("tol", ctypes.c_double)]
+                ("tol", ctypes.c_double), ("precond", ctypes.c_int32)]
 
 
 class ie_solve_stats(ctypes.Structure):
@@ -265,9 +265,9 @@ def ie_apply_operator(ctx, x, y, box=None):
     _check(ctx, _lib.ie_apply_operator(ctx.handle, _box(box), int(nrhs), _ptr(x), _ptr(y)), "ie_apply_operator")
 
 
-def ie_solve_subdomain(ctx, b, x, tol, restart=30, max_iters=5000, min_iters=0, box=None, check=True):
+def ie_solve_subdomain(ctx, b, x, tol, restart=30, max_iters=5000, min_iters=0, box=None, check=True, precond=0):
     nrhs = b.shape[0] if b.dim() == 5 else 1
-    o = ie_gmres_opts(int(restart), int(max_iters), int(min_iters), float(tol))
+    o = ie_gmres_opts(int(restart), int(max_iters), int(min_iters), float(tol), int(precond))
     st = (ie_solve_stats * nrhs)()
     s = _lib.ie_solve_subdomain(ctx.handle, _box(box), int(nrhs), _ptr(b), _ptr(x), ctypes.byref(o), st)
     stats = [dict(iters=t.iters, restarts=t.restarts, converged=bool(t.converged), relres_est=t.relres_est,
@@ -279,14 +279,14 @@ def ie_solve_subdomain(ctx, b, x, tol, restart=30, max_iters=5000, min_iters=0, 
 
 def ie_solve_dd(ctx, e, scheme, boxes=(), outer_tol=1e-8, adaptive=True, inner_tol_fixed=1e-6,
                 inner_tol_factor=0.1, max_sweeps=200, restart=30, max_iters=2000, min_iters=1,
-                init_from_e=False, check=True):
+                init_from_e=False, check=True, precond=0):
     """Algorithm 1 (or full-domain GMRES for scheme="full").  e: [n_src][3][nz][ny][nx] CUDA tensor."""
     ns = ctx.n_src
     nb = len(boxes)
     arr = (ie_box * max(nb, 1))(*[ie_box(*[int(v) for v in b]) for b in boxes])
     o = ie_dd_opts(SCHEMES[scheme] if isinstance(scheme, str) else int(scheme), arr, nb, float(outer_tol),
                    int(bool(adaptive)), float(inner_tol_fixed), float(inner_tol_factor), int(max_sweeps),
-                   ie_gmres_opts(int(restart), int(max_iters), int(min_iters), 0.0))
+                   ie_gmres_opts(int(restart), int(max_iters), int(min_iters), 0.0, int(precond)))
     e_hist = np.zeros(((max_sweeps + 1), ns), np.float64)
     iters = np.zeros((max(max_sweeps, 1), max(nb, 1), ns), np.int32)
     st = ie_dd_stats(0, 0, 0, 0, 0.0, e_hist.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),

@@ -47,6 +47,22 @@ static ie_box full_box(const ie_ctx* c) { return ie_box{0, c->g.nx, 0, c->g.ny, 
 static const double* dsig_at(const ie_ctx* c, const ie_box& b) {
   return c->dsig + ((long long)b.k0 * c->g.ny + b.j0) * c->g.nx + b.i0;
 }
+static const double* at_box(const ie_ctx* c, const double* grid6, const ie_box& b) {
+  return grid6 + ((long long)b.k0 * c->g.ny + b.j0) * c->g.nx + b.i0;
+}
+
+// a GMRES system on box b; with the contraction-IE right preconditioner (opts precond = 1)
+// the operator is (I - G dsigma) P, P = 2 sigma_b (sigma + sigma_b I)^-1
+static GmresSystem make_sys(const ie_ctx* c, const double2* b_, double2* x_, const ie_box& b, double tol,
+                            int min_iters, int precond) {
+  GmresSystem s{b_, x_, dsig_at(c, b), tol, min_iters};
+  if (precond) {
+    s.dsig = at_box(c, c->pre_dp, b);
+    s.pm = at_box(c, c->pre_p, b);
+    s.pa = at_box(c, c->pre_a, b);
+  }
+  return s;
+}
 
 // Apply on a box-shaped domain for nitems inputs (x[i] compact over the source sub-box src,
 // which is relative to the domain box).  y = alpha x + beta G dsigma x (+ y).
@@ -210,6 +226,7 @@ ie_status ie_destroy(ie_ctx* c) {
   }
   cudaFree(c->tab);
   cudaFree(c->dsig);
+  cudaFree(c->pre_p);
   cudaFree(c->e0);
   cudaFree(c->tw.dev);
   cudaFree(c->d_red);
@@ -322,6 +339,11 @@ ie_status ie_solve_subdomain(ie_ctx* c, const ie_box* box, int32_t nrhs, const v
   if (!c || nrhs < 1 || !b_dev || !x_dev || !o || !stats || o->restart < 1 || o->restart > 128 || !(o->tol > 0))
     return fail(c, IE_ERR_INVALID_ARGUMENT, "solve_subdomain: bad arguments");
   if (!c->contrast_set) return fail(c, IE_ERR_STATE, "solve before set_contrast");
+  if (o->precond < 0 || o->precond > 1) return fail(c, IE_ERR_INVALID_ARGUMENT, "solve_subdomain: precond 0 or 1");
+  if (o->precond) {
+    ie_status sp = ensure_precond(c);
+    if (sp) return sp;
+  }
   const ie_box b = box ? *box : full_box(c);
   std::string why;
   if (!box_ok(c, b, &why)) return fail(c, IE_ERR_INVALID_ARGUMENT, why);
@@ -329,8 +351,8 @@ ie_status ie_solve_subdomain(ie_ctx* c, const ie_box* box, int32_t nrhs, const v
   const long long nb = 3LL * bx * by * bz;
   std::vector<GmresSystem> sys;
   for (int r = 0; r < nrhs; ++r)
-    sys.push_back(GmresSystem{(const double2*)b_dev + r * nb, (double2*)x_dev + r * nb, dsig_at(c, b), o->tol,
-                              o->min_iters});
+    sys.push_back(make_sys(c, (const double2*)b_dev + r * nb, (double2*)x_dev + r * nb, b, o->tol, o->min_iters,
+                           o->precond));
   Arena ar = arena_of(c);
   std::vector<GmresResult> res;
   ie_status st = gmres_batched(c, ar, bx, by, bz, b.k0, (long long)c->g.nx * c->g.ny, c->g.nx, sys, o->restart,
@@ -356,8 +378,13 @@ ie_status ie_solve_subdomain(ie_ctx* c, const ie_box* box, int32_t nrhs, const v
 ie_status ie_solve_dd(ie_ctx* c, const ie_dd_opts* o, void* e_dev, int32_t init_from_e, ie_dd_stats* stats) {
   if (!c || !o || !e_dev || !stats) return fail(c, IE_ERR_INVALID_ARGUMENT, "solve_dd: bad arguments");
   if (!c->contrast_set || !c->e0 || c->n_src < 1) return fail(c, IE_ERR_STATE, "solve_dd needs contrast and sources");
-  if (o->inner.restart < 1 || o->inner.restart > 128 || !(o->outer_tol > 0) || o->max_sweeps < 0)
+  if (o->inner.restart < 1 || o->inner.restart > 128 || !(o->outer_tol > 0) || o->max_sweeps < 0 ||
+      o->inner.precond < 0 || o->inner.precond > 1)
     return fail(c, IE_ERR_INVALID_ARGUMENT, "solve_dd: bad options");
+  if (o->inner.precond) {
+    ie_status sp = ensure_precond(c);
+    if (sp) return sp;
+  }
   const int ns = c->n_src;
   const long long N = ncell(c), len = 3 * N;
   double2* E = (double2*)e_dev;
@@ -374,7 +401,7 @@ ie_status ie_solve_dd(ie_ctx* c, const ie_dd_opts* o, void* e_dev, int32_t init_
   if (o->scheme == IE_DD_FULL) {
     std::vector<GmresSystem> sys;
     for (int r = 0; r < ns; ++r)
-      sys.push_back(GmresSystem{c->e0 + r * len, E + r * len, c->dsig, o->outer_tol, o->inner.min_iters});
+      sys.push_back(make_sys(c, c->e0 + r * len, E + r * len, fb, o->outer_tol, o->inner.min_iters, o->inner.precond));
     std::vector<GmresResult> res;
     long long ap = 0;
     ie_status st = gmres_batched(c, ar, c->g.nx, c->g.ny, c->g.nz, 0, (long long)c->g.nx * c->g.ny, c->g.nx, sys, m,
@@ -503,8 +530,8 @@ ie_status ie_solve_dd(ie_ctx* c, const ie_dd_opts* o, void* e_dev, int32_t init_
     for (int i : ids)
       for (int r : rr) {
         const double thr = o->adaptive ? e[r] * o->inner_tol_factor : o->inner_tol_fixed;
-        sys.push_back(GmresSystem{Bb + boff[i] + r * nbox(i), Xb + boff[i] + r * nbox(i), dsig_at(c, o->boxes[i]), thr,
-                                  std::max(1, o->inner.min_iters)});
+        sys.push_back(make_sys(c, Bb + boff[i] + r * nbox(i), Xb + boff[i] + r * nbox(i), o->boxes[i], thr,
+                               std::max(1, o->inner.min_iters), o->inner.precond));
         who.push_back({i, r});
       }
     std::vector<GmresResult> res;

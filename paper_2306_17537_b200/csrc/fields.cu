@@ -79,6 +79,10 @@ ie_status pack_contrast(ie_ctx* c, const void* sigma_dev, int layout) {
   if (e) return cuda_fail(c, e, "set_contrast");
   if (hbad) return fail(c, IE_ERR_INVALID_ARGUMENT, "sigma is not symmetric to 1e-12 (P:415) or not finite");
   c->contrast_set = true;
+  if (c->pre_p) {  // a new contrast invalidates the preconditioner (rebuilt on next use)
+    cudaFree(c->pre_p);
+    c->pre_p = c->pre_a = c->pre_dp = nullptr;
+  }
   return IE_OK;
 }
 
@@ -323,6 +327,89 @@ __global__ void k_axpby(double2* __restrict__ z, double2 a, const double2* __res
 void launch_axpby(ie_ctx* c, double2* z, cplx a, const double2* x, cplx b, const double2* y, long long n) {
   k_axpby<<<grid_for(n, 256, 148 * 8), 256, 0, c->stream>>>(z, make_double2(a.real(), a.imag()), x,
                                                            make_double2(b.real(), b.imag()), y, n);
+  c->launches++;
+}
+
+// ---------------------------------------- contraction-IE right preconditioner
+// Per cell, from dsigma (sym6) and sigma_b(z):  a = (sigma + sigma_b I) / (2 sigma_b),
+// P = a^-1 = 2 sigma_b (sigma + sigma_b I)^-1 and dsigma P (a function of the same symmetric
+// matrix as dsigma, hence symmetric).  The change of unknown chi = a E turns Eq. 8 into
+// (I - G dsigma) P chi = E0 with the same Eq. 9 residual (Hursan & Zhdanov's contraction IE as
+// a right preconditioner).
+__global__ void k_precond_build(const double* __restrict__ ds, double* __restrict__ pa, double* __restrict__ pp,
+                                double* __restrict__ pdp, long long N, long long nxy, double sb0,
+                                const double* __restrict__ sbz) {
+  for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < N; c += (long long)gridDim.x * blockDim.x) {
+    const double sb = sbz ? sbz[c / nxy] : sb0;
+    const double d[6] = {ds[c], ds[N + c], ds[2 * N + c], ds[3 * N + c], ds[4 * N + c], ds[5 * N + c]};
+    // a = (dsigma + 2 sigma_b I) / (2 sigma_b)  (sigma + sigma_b I = dsigma + 2 sigma_b I)
+    const double s = 0.5 / sb;
+    const double a0 = (d[0] + 2 * sb) * s, a1 = (d[1] + 2 * sb) * s, a2 = (d[2] + 2 * sb) * s;
+    const double a3 = d[3] * s, a4 = d[4] * s, a5 = d[5] * s;  // xy, xz, yz
+    // symmetric inverse by cofactors
+    const double c00 = a1 * a2 - a5 * a5, c11 = a0 * a2 - a4 * a4, c22 = a0 * a1 - a3 * a3;
+    const double c01 = a4 * a5 - a3 * a2, c02 = a3 * a5 - a1 * a4, c12 = a3 * a4 - a0 * a5;
+    const double inv = 1.0 / (a0 * c00 + a3 * c01 + a4 * c02);
+    const double p[6] = {c00 * inv, c11 * inv, c22 * inv, c01 * inv, c02 * inv, c12 * inv};
+    const double A[6] = {a0, a1, a2, a3, a4, a5};
+    // dsigma P, symmetrised (equal to P dsigma in exact arithmetic)
+    auto m = [](const double* x, int i, int j) {
+      const int idx[3][3] = {{0, 3, 4}, {3, 1, 5}, {4, 5, 2}};
+      return x[idx[i][j]];
+    };
+    double dp[3][3];
+    for (int i = 0; i < 3; ++i)
+      for (int j = 0; j < 3; ++j) dp[i][j] = m(d, i, 0) * m(p, 0, j) + m(d, i, 1) * m(p, 1, j) + m(d, i, 2) * m(p, 2, j);
+    const double q[6] = {dp[0][0], dp[1][1], dp[2][2], 0.5 * (dp[0][1] + dp[1][0]), 0.5 * (dp[0][2] + dp[2][0]),
+                         0.5 * (dp[1][2] + dp[2][1])};
+    for (int k = 0; k < 6; ++k) {
+      pa[k * N + c] = A[k];
+      pp[k * N + c] = p[k];
+      pdp[k * N + c] = q[k];
+    }
+  }
+}
+
+ie_status ensure_precond(ie_ctx* c) {
+  if (c->pre_p) return IE_OK;
+  if (!c->contrast_set) return fail(c, IE_ERR_STATE, "preconditioner needs the contrast");
+  const long long N = (long long)c->g.nx * c->g.ny * c->g.nz;
+  IE_CUDA(c, cudaMalloc(&c->pre_p, 3 * 6 * N * sizeof(double)));
+  c->pre_a = c->pre_p + 6 * N;
+  c->pre_dp = c->pre_p + 12 * N;
+  double* sbz = nullptr;
+  std::vector<double> hsb;
+  if (c->layered) {
+    for (int k = 0; k < c->g.nz; ++k) hsb.push_back(sigma_b_at(c, k));
+    IE_CUDA(c, cudaMalloc(&sbz, hsb.size() * sizeof(double)));
+    IE_CUDA(c, cudaMemcpyAsync(sbz, hsb.data(), hsb.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  }
+  k_precond_build<<<grid_for(N, 256), 256, 0, c->stream>>>(c->dsig, c->pre_a, c->pre_p, c->pre_dp, N,
+                                                           (long long)c->g.nx * c->g.ny, c->sigma_b, sbz);
+  IE_CHECK_LAUNCH(c, "k_precond_build");
+  IE_CUDA(c, cudaStreamSynchronize(c->stream));
+  cudaFree(sbz);
+  return IE_OK;
+}
+
+// y = M x per cell; M sym6 over the grid (strides cs, zs, ys), x and y compact over the box
+__global__ void k_cellmat(double2* __restrict__ y, const double2* __restrict__ x, const double* __restrict__ M, int bx,
+                          int by, int bz, long long cs, long long zs, long long ys) {
+  const long long Nb = (long long)bx * by * bz;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < Nb; i += (long long)gridDim.x * blockDim.x) {
+    const int ix = (int)(i % bx), iy = (int)((i / bx) % by), iz = (int)(i / ((long long)bx * by));
+    const double* m = M + iz * zs + iy * ys + ix;
+    const double m0 = m[0], m1 = m[cs], m2 = m[2 * cs], m3 = m[3 * cs], m4 = m[4 * cs], m5 = m[5 * cs];
+    const double2 x0 = x[i], x1 = x[Nb + i], x2 = x[2 * Nb + i];
+    y[i] = make_double2(m0 * x0.x + m3 * x1.x + m4 * x2.x, m0 * x0.y + m3 * x1.y + m4 * x2.y);
+    y[Nb + i] = make_double2(m3 * x0.x + m1 * x1.x + m5 * x2.x, m3 * x0.y + m1 * x1.y + m5 * x2.y);
+    y[2 * Nb + i] = make_double2(m4 * x0.x + m5 * x1.x + m2 * x2.x, m4 * x0.y + m5 * x1.y + m2 * x2.y);
+  }
+}
+void launch_cellmat(ie_ctx* c, double2* y, const double2* x, const double* M, int bx, int by, int bz, long long cs,
+                    long long zs, long long ys) {
+  const long long Nb = (long long)bx * by * bz;
+  k_cellmat<<<grid_for(Nb, 256, 148 * 8), 256, 0, c->stream>>>(y, x, M, bx, by, bz, cs, zs, ys);
   c->launches++;
 }
 

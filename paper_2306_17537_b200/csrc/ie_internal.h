@@ -28,7 +28,9 @@ constexpr int kMaxLog2 = 10;         // FFT lengths 2 .. 1024
 struct ApplyItem {
   const double2* x;    // [3][sz][sy][sx] over the source sub-box
   double2* y;          // [3][nz][ny][nx] over the domain
-  const double* dsig;  // sym6 dsigma at domain cell (0,0,0); strides in ApplyParams
+  const double* dsig;  // sym6 dsigma (or dsigma P) at domain cell (0,0,0); strides in ApplyParams
+  const double* pm;    // contraction-IE right preconditioner P (sym6, same strides) or null:
+                       // the identity term becomes P x (the operator applied is (I - G dsigma) P)
   double xscale;
   int sx0, sx1, sy0, sy1, sz0, sz1;
 };
@@ -95,6 +97,10 @@ struct ie_ctx {
   int n_src = 0;
   std::vector<double> src_pos, src_mom;  // host copies of the dipoles (for H0 at receivers)
   bool contrast_set = false;
+  // contraction-IE right preconditioner, built on first use: sym6 [6][N] each
+  double* pre_p = nullptr;   // P = 2 sigma_b (sigma + sigma_b I)^-1
+  double* pre_a = nullptr;   // a = P^-1
+  double* pre_dp = nullptr;  // dsigma P
   char* ws = nullptr;
   size_t ws_bytes = 0;
   std::string err;
@@ -171,6 +177,10 @@ void launch_gather(ie_ctx* c, const double2* full, double2* box, const ie_box& b
 void launch_scatter(ie_ctx* c, double2* full, const double2* box, const ie_box& b, int nsys, long long full_stride,
                     long long box_stride);
 void launch_axpby(ie_ctx* c, double2* z, cplx a, const double2* x, cplx b, const double2* y, long long n);
+ie_status ensure_precond(ie_ctx* c);
+// y = M x per cell (M sym6 over the grid with strides (cs, zs, ys), x, y compact [3][bz][by][bx])
+void launch_cellmat(ie_ctx* c, double2* y, const double2* x, const double* M, int bx, int by, int bz, long long cs,
+                    long long zs, long long ys);
 // sums of |a - b|^2 (b may be null) per system; result doubles on host
 ie_status norms2(ie_ctx* c, const double2* a, const double2* b, int nsys, long long len, long long stride,
                  double* out_host);
@@ -178,9 +188,11 @@ ie_status norms2(ie_ctx* c, const double2* a, const double2* b, int nsys, long l
 struct GmresSystem {
   const double2* b;  // rhs (compact over the domain)
   double2* x;        // initial guess in, solution out
-  const double* dsig;
+  const double* dsig;  // dsigma, or dsigma P when preconditioned
   double tol;
   int min_iters;
+  const double* pm = nullptr;  // right preconditioner P = 2 sigma_b (sigma + sigma_b I)^-1 (sym6) or null
+  const double* pa = nullptr;  // its inverse a = (sigma + sigma_b I) / (2 sigma_b): chi0 = a x0
 };
 struct GmresResult {
   int iters = 0, restarts = 0, converged = 0, breakdown = 0;

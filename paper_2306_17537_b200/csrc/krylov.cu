@@ -250,6 +250,7 @@ ie_status gmres_batched(ie_ctx* c, Arena& ar, int nx, int ny, int nz, int k0, lo
         it.x = xin[b0 + i];
         it.y = yout[b0 + i];
         it.dsig = sys[ids[b0 + i]].dsig;
+        it.pm = sys[ids[b0 + i]].pm;
         it.xscale = xsc[b0 + i];
         it.sx0 = 0;
         it.sx1 = nx;
@@ -300,6 +301,10 @@ ie_status gmres_batched(ie_ctx* c, Arena& ar, int nx, int ny, int nz, int k0, lo
     IE_CHECK_LAUNCH(c, "k_maxpy");
     return IE_OK;
   };
+
+  // right preconditioning (contraction IE): iterate on chi = a x, return x = P chi
+  for (int s = 0; s < S; ++s)
+    if (sys[s].pa) launch_cellmat(c, sys[s].x, sys[s].x, sys[s].pa, nx, ny, nz, ap.ds_cs, ds_zs, ds_ys);
 
   std::vector<SysState> ss(S);
   for (auto& s : ss) {
@@ -517,6 +522,8 @@ ie_status gmres_batched(ie_ctx* c, Arena& ar, int nx, int ny, int nz, int k0, lo
       }
     }
   }
+  for (int s = 0; s < S; ++s)
+    if (sys[s].pm) launch_cellmat(c, sys[s].x, sys[s].x, sys[s].pm, nx, ny, nz, ap.ds_cs, ds_zs, ds_ys);
   return IE_OK;
 }
 

@@ -488,6 +488,10 @@ __global__ void __launch_bounds__(128) k_xinv(const __grid_constant__ ApplyParam
   const double a = p.alpha * it.xscale, b = p.beta;
   double2* yrow = it.y + l * N + off;
   const double2* xrow = it.x + l * N + off;
+  // contraction-IE right preconditioner: the identity term is (P x)_l (row l of sym6 P)
+  const int pc0 = l == 0 ? 0 : (l == 1 ? 3 : 4), pc1 = l == 0 ? 3 : (l == 1 ? 1 : 5), pc2 = l == 0 ? 4 : (l == 1 ? 5 : 2);
+  const double* prow = it.pm ? it.pm + zz * p.ds_zs + yy * p.ds_ys : nullptr;
+  const double2* x0row = it.x + off;
 #pragma unroll
   for (int u = 0; u < V / RL; ++u)
 #pragma unroll
@@ -495,7 +499,15 @@ __global__ void __launch_bounds__(128) k_xinv(const __grid_constant__ ApplyParam
       const int x = t + u * T + r * (L / RL);
       double2 o = cscale(v[0][u * RL + r], b);
       if (a != 0.0) {
-        const double2 xi = ld2(xrow + x);
+        double2 xi;
+        if (prow) {
+          const double q0 = __ldg(prow + pc0 * p.ds_cs + x), q1 = __ldg(prow + pc1 * p.ds_cs + x),
+                       q2 = __ldg(prow + pc2 * p.ds_cs + x);
+          const double2 e0 = ld2(x0row + x), e1 = ld2(x0row + N + x), e2 = ld2(x0row + 2 * N + x);
+          xi = make_double2(q0 * e0.x + q1 * e1.x + q2 * e2.x, q0 * e0.y + q1 * e1.y + q2 * e2.y);
+        } else {
+          xi = ld2(xrow + x);
+        }
         o.x = fma(a, xi.x, o.x);
         o.y = fma(a, xi.y, o.y);
       }

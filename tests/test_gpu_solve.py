@@ -149,3 +149,50 @@ def test_c2mod_solves_match_oracle_gmres(scheme):
     H, _ = ie.ie_receiver_fields(ctx, e, np.array(cfg.receivers))
     Href = orx.receiver_H(cfg.n, cfg.hvec, cfg.origin, k0, cfg.sigma_b, ds, Xref, cfg.receivers, *cfg.sources[0])
     assert rel(H[0], Href) < FIELD_TOL
+
+
+@pytest.mark.parametrize("name", ["c1", "c2mini", "c3mini", "c5mini"])
+@pytest.mark.parametrize("scheme", ["full", "jacobi", "gauss_seidel"])
+def test_contraction_preconditioned_solves_match_dense_lu(name, scheme):
+    """Right preconditioner P = 2 sigma_b (sigma + sigma_b I)^-1 (contraction IE):
+    the same discrete solution (dense LU) and the same Eq. 9 residual."""
+    import paper_2306_17537_b200 as ie
+    cfg = make_config(name)
+    ctx, sigma = gpu_ctx(cfg)
+    k0, ds, E0, X = _lu_truth(cfg, sigma)
+    e = _field(cfg, len(cfg.sources))
+    st = ie.ie_solve_dd(ctx, e, scheme, boxes=cfg.boxes, outer_tol=1e-9, restart=cfg.restart, precond=1)
+    assert st["e_final"] <= 1e-9
+    assert rel(e.cpu().numpy(), X) < FIELD_TOL
+
+
+def test_contraction_preconditioned_subdomain_solve_on_a_box():
+    import torch
+    import paper_2306_17537_b200 as ie
+    cfg = make_config("c2mini")
+    ctx, sigma = gpu_ctx(cfg)
+    k0, ds, E0, _ = _lu_truth(cfg, sigma)
+    box = (0, 8, 0, 8, 2, 6)
+    Ab = op.dense_matrix((8, 8, 4), cfg.hvec, k0, cfg.sigma_b, ds[2:6])
+    rng = np.random.default_rng(8)
+    bb = rng.standard_normal((1, 3, 4, 8, 8)) + 1j * rng.standard_normal((1, 3, 4, 8, 8))
+    b = torch.from_numpy(bb).cuda()
+    x = b.clone()
+    stats, _ = ie.ie_solve_subdomain(ctx, b, x, tol=1e-10, restart=30, box=box, precond=1)
+    assert stats[0]["converged"] and stats[0]["relres_true"] <= 1e-10
+    ref = np.linalg.solve(Ab, bb[0].ravel()).reshape(bb[0].shape)
+    assert rel(x.cpu().numpy()[0], ref) < FIELD_TOL
+
+
+@pytest.mark.parametrize("scheme", ["full", "gauss_seidel"])
+def test_c2mod_preconditioned_matches_oracle_gmres(scheme):
+    import paper_2306_17537_b200 as ie
+    cfg = make_config("c2mod")
+    ctx, sigma = gpu_ctx(cfg)
+    k0, ds, E0 = oracle_setup(cfg, sigma)
+    Aop = op.Operator(cfg.n, cfg.hvec, k0, cfg.sigma_b, ds)
+    Xref, info = gmres(Aop, E0[0], x0=E0[0], tol=1e-12, restart=30, max_iters=3000)
+    assert info["converged"]
+    e = _field(cfg, 1)
+    st = ie.ie_solve_dd(ctx, e, scheme, boxes=cfg.boxes, outer_tol=1e-9, restart=30, max_sweeps=300, precond=1)
+    assert rel(e.cpu().numpy()[0], Xref) < FIELD_TOL
