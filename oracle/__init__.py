@@ -17,4 +17,4 @@ by a ``-m "not gpu"`` test in ``tests/test_oracle_*.py`` except where its docstr
 "parity unpinned".
 """
 
-from . import physics, operator, gmres, dd, receivers, layered  # noqa: F401
+from . import physics, operator, gmres, dd, receivers, layered, preconditioner  # noqa: F401

@@ -78,3 +78,31 @@ def test_born_limit_second_order():
         rem.append(np.linalg.norm(E - born))
     ratio = rem[0] / rem[1]
     assert 80 < ratio < 125
+
+
+def test_contraction_preconditioner_algebra_and_solution_invariance():
+    """P a = I; isotropic sigma gives the scalar 2 sigma_b / (sigma + sigma_b); GMRES on
+    (I - G dsigma) P chi = E0 returns E = P chi equal to the dense LU solution."""
+    from oracle import preconditioner as pc
+    cfg = make_config("c2mini")
+    sigma = cfg.sigma()
+    P = pc.contraction_P(sigma, cfg.sigma_b)
+    a = (sigma + cfg.sigma_b * np.eye(3)) / (2 * cfg.sigma_b)
+    assert np.abs(np.einsum("...ij,...jk->...ik", P, a) - np.eye(3)).max() < 1e-13
+    s_iso = np.eye(3) * 0.7
+    assert np.allclose(pc.contraction_P(s_iso, 0.1), 2 * 0.1 / (0.7 + 0.1) * np.eye(3), rtol=1e-15)
+    k0 = physics.wavenumber(cfg.sigma_b, cfg.freq)
+    ds = physics.contrast(sigma, cfg.sigma_b)
+    pts = physics.centroids(cfg.n, cfg.hvec, cfg.origin)
+    E0 = np.moveaxis(physics.incident_E(pts, *cfg.sources[0], k0, cfg.freq), -1, 0)
+    A = op.Operator(cfg.n, cfg.hvec, k0, cfg.sigma_b, ds)
+    X = np.linalg.solve(op.dense_matrix(cfg.n, cfg.hvec, k0, cfg.sigma_b, ds), E0.ravel()).reshape(E0.shape)
+
+    class AP:
+        def __call__(self, chi):
+            return A(pc.apply_cellwise(P, chi))
+    chi, info = gmres(AP(), E0, x0=pc.apply_cellwise(a, E0), tol=1e-12, restart=30)
+    assert info["converged"]
+    E = pc.apply_cellwise(P, chi)
+    assert np.linalg.norm(E - X) < 1e-9 * np.linalg.norm(X)
+    assert np.linalg.norm(E0 - A(E)) / np.linalg.norm(E0) < 1e-11  # the Eq. 9 residual
