@@ -82,7 +82,7 @@ static ie_status apply_many(ie_ctx* c, Arena& ar, const ie_box& dom, const ie_bo
     return fail(c, IE_ERR_OUT_OF_MEMORY, "workspace too small for the operator (need " + std::to_string(ar.peak) +
                                              " bytes; see ie_workspace_query)");
   }
-  ApplyParams p;
+  ApplyParams p{};
   p.nx = bx;
   p.ny = by;
   p.nz = bz;
@@ -104,6 +104,7 @@ static ie_status apply_many(ie_ctx* c, Arena& ar, const ie_box& dom, const ie_bo
       it.x = x[b0 + i];
       it.y = y[b0 + i];
       it.dsig = dsig_at(c, dom);
+      it.pm = nullptr;
       it.xscale = 1.0;
       it.sx0 = src.i0;
       it.sx1 = src.i1;

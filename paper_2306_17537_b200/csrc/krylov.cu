@@ -225,7 +225,7 @@ ie_status gmres_batched(ie_ctx* c, Arena& ar, int nx, int ny, int nz, int k0, lo
 
   auto Vs = [&](int s, int j) { return V + ((long long)s * (m + 1) + j) * len; };
 
-  ApplyParams ap;
+  ApplyParams ap{};
   ap.nx = nx;
   ap.ny = ny;
   ap.nz = nz;
