@@ -422,6 +422,14 @@ def run_ours(args, cfg, sigma, rank, ws, local):
     cufft = None if args.no_cufft else cufft_reference(ctx, cfg, sigma, x)
     layered = None if args.no_layered else layered_leg()
     sweep = None if args.no_sweep else c4_sweep()
+    window = None
+    if not args.no_window:  # the paper's moving-window logging (section 3.3)
+        sys.path.insert(0, os.path.join(ROOT, "tools"))
+        import logging_window
+        window = {sch: logging_window.run(3, scheme=sch) for sch in ("gauss_seidel", "full")}
+        for w in window.values():
+            w["paper_context"] = "window 1 (128x128x256 cells), GS-A tol 1e-3: ~1.5 min per position on an " \
+                                 "RTX 3060 Laptop with MATLAB (P:287)"
 
     # --- forward solve seconds per tool position (full-domain GMRES vs DD schemes)
     dd = None
@@ -458,7 +466,7 @@ def run_ours(args, cfg, sigma, rank, ws, local):
                        "status": ie.STATUS.get(st["status"], st["status"])}
     return dict(value=value, per_step=per_step, launches=launches, clk=clk.summary(), peak=peak,
                 peak_src=peak_src, dom=dom, achieved=achieved, kernels=kernels, e2e=e2e, dd=dd, bm=bm, cufft=cufft,
-                layered=layered, sweep=sweep,
+                layered=layered, sweep=sweep, window=window,
                 traffic=args.traffic)
 
 
@@ -475,6 +483,7 @@ def main():
     ap.add_argument("--no-cufft", action="store_true")
     ap.add_argument("--no-layered", action="store_true")
     ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--no-window", action="store_true")
     ap.add_argument("--traffic", type=float, default=None, help="ncu dram bytes per launch of the dominant kernel")
     args = ap.parse_args()
     assert args.warmup >= 3 or args.impl == "reference" or args.warmup >= 0
@@ -515,7 +524,7 @@ def main():
             "kernels": r["kernels"],
             "e2e": r["e2e"], "gpu_launches": r["launches"], "clocks": r["clk"],
             "cpu_baseline": cpu, "cufft_reference": r["cufft"], "layered": r["layered"], "dd": r["dd"],
-            "logging_sweep": r["sweep"]}
+            "logging_sweep": r["sweep"], "moving_window_logging": r["window"]}
     print(json.dumps(line))
 
 

@@ -89,3 +89,24 @@ def test_c4_stations_inside_grid():
 def test_box_grid_order():
     b = box_grid((8, 4, 2), (2, 2, 1))
     assert b[0] == (0, 4, 0, 2, 0, 2) and b[1] == (4, 8, 0, 2, 0, 2) and b[2] == (0, 4, 2, 4, 0, 2)
+
+
+def test_logging_formation_and_window_rotation():
+    """Formation tensors are symmetric positive definite; a window tensor is R^T sigma R of the
+    formation at the mapped centroid (checked at one cell); sand cells are isotropic (Eq. 25)."""
+    from ie_workloads import logging as lg
+    n, h = (8, 4, 4), 1.0
+    tx = lg.stations(4)[2]
+    s = lg.window_sigma(tx, n, h, behind=3.0)
+    assert np.abs(s - np.swapaxes(s, -1, -2)).max() < 1e-15
+    assert np.linalg.eigvalsh(s).min() > 0
+    origin, R = lg.window_grid(n, h, behind=3.0)
+    i, j, k = 5, 1, 2
+    r = tx + R @ (origin + h * np.array([i, j, k]))
+    ref = R.T @ lg.formation_sigma(r[None])[0] @ R
+    assert np.abs(s[k, j, i] - ref).max() < 1e-14
+    assert abs(np.linalg.det(R) - 1) < 1e-14 and abs(R[:, 0] @ lg.hole_direction() - 1) < 1e-14
+    # a sand point (Eq. 25): isotropic, perturbation peak at r_c
+    z_sand = 0.5 * (lg.BEDS[5][0] + lg.BEDS[6][0]) + lg.bed_shift(500.0)
+    sp = lg.formation_sigma(np.array([[500.0, 0.0, z_sand]]))[0]
+    assert np.allclose(sp, sp[0, 0] * np.eye(3))
