@@ -173,7 +173,17 @@ typedef struct {
 ie_status ie_solve_subdomain(ie_ctx* ctx, const ie_box* box, int32_t nrhs, const void* b_dev, void* x_dev,
                              const ie_gmres_opts* opts, ie_solve_stats* stats);
 
-typedef enum { IE_DD_FULL = 0, IE_DD_JACOBI = 1, IE_DD_GAUSS_SEIDEL = 2 } ie_dd_scheme;
+/* IE_DD_FGMRES_*: Krylov-accelerated DD (the paper's future work):
+ * flexible GMRES(10) on the full system, right-preconditioned by one block-Jacobi or block
+ * Gauss-Seidel sweep from zero with inner GMRES to inner_tol_fixed; max_sweeps caps the outer
+ * (preconditioned) iterations, adaptive / inner_tol_factor are unused. */
+typedef enum {
+  IE_DD_FULL = 0,
+  IE_DD_JACOBI = 1,
+  IE_DD_GAUSS_SEIDEL = 2,
+  IE_DD_FGMRES_JACOBI = 3,
+  IE_DD_FGMRES_GAUSS_SEIDEL = 4
+} ie_dd_scheme;
 
 /* Algorithm 1 options.  boxes: a non-overlapping partition of the grid (Eq. 11), host
  * array; Gauss-Seidel visits them in the given order (reading R12).  The inner GMRES

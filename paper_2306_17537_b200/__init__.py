@@ -21,8 +21,9 @@ IE_OK = 0
 STATUS = {0: "IE_OK", 1: "IE_ERR_INVALID_ARGUMENT", 2: "IE_ERR_OUT_OF_MEMORY", 3: "IE_ERR_CUDA",
           4: "IE_ERR_NOT_CONVERGED", 5: "IE_ERR_BREAKDOWN", 6: "IE_ERR_STATE", 7: "IE_ERR_PLACEMENT",
           8: "IE_ERR_UNSUPPORTED"}
-IE_DD_FULL, IE_DD_JACOBI, IE_DD_GAUSS_SEIDEL = 0, 1, 2
-SCHEMES = {"full": IE_DD_FULL, "jacobi": IE_DD_JACOBI, "gauss_seidel": IE_DD_GAUSS_SEIDEL}
+IE_DD_FULL, IE_DD_JACOBI, IE_DD_GAUSS_SEIDEL, IE_DD_FGMRES_JACOBI, IE_DD_FGMRES_GAUSS_SEIDEL = 0, 1, 2, 3, 4
+SCHEMES = {"full": IE_DD_FULL, "jacobi": IE_DD_JACOBI, "gauss_seidel": IE_DD_GAUSS_SEIDEL,
+           "fgmres_jacobi": IE_DD_FGMRES_JACOBI, "fgmres_gauss_seidel": IE_DD_FGMRES_GAUSS_SEIDEL}
 
 EXPORTED = ("ie_create", "ie_destroy", "ie_last_error", "ie_workspace_query", "ie_bind_workspace",
             "ie_set_contrast", "ie_set_source", "ie_get_incident", "ie_set_incident", "ie_apply_operator",

@@ -28,6 +28,7 @@ ie_status cuda_fail(ie_ctx* c, cudaError_t e, const char* where) {
 }
 
 static long long ncell(const ie_ctx* c) { return (long long)c->g.nx * c->g.ny * c->g.nz; }
+constexpr int kFgmresRestart = 10;  // outer FGMRES restart of the Krylov-accelerated DD
 
 static bool box_ok(const ie_ctx* c, const ie_box& b, std::string* why) {
   if (b.i0 < 0 || b.j0 < 0 || b.k0 < 0 || b.i1 > c->g.nx || b.j1 > c->g.ny || b.k1 > c->g.nz || b.i1 <= b.i0 ||
@@ -130,6 +131,7 @@ static Arena arena_of(ie_ctx* c) {
 static size_t dd_bytes(int nx, int ny, int nz, const ie_box* boxes, int n_boxes, int ns, int m) {
   const size_t len = 3ull * nx * ny * nz;
   size_t fixed = 2 * (size_t)ns * len * sizeof(double2) + 3 * (size_t)ns * len * sizeof(double2) + 8192;
+  fixed += (2 * kFgmresRestart + 1) * len * sizeof(double2) + 65536;  // Krylov-accelerated DD basis
   // largest same-shape group (Jacobi batch) and any single box (GS)
   std::map<std::vector<int>, int> groups;
   for (int i = 0; i < n_boxes; ++i)
@@ -421,7 +423,8 @@ ie_status ie_solve_dd(ie_ctx* c, const ie_dd_opts* o, void* e_dev, int32_t init_
     if (!allc) return fail(c, IE_ERR_NOT_CONVERGED, "full-domain GMRES reached max_iters");
     return IE_OK;
   }
-  if (o->scheme != IE_DD_JACOBI && o->scheme != IE_DD_GAUSS_SEIDEL)
+  if (o->scheme != IE_DD_JACOBI && o->scheme != IE_DD_GAUSS_SEIDEL && o->scheme != IE_DD_FGMRES_JACOBI &&
+      o->scheme != IE_DD_FGMRES_GAUSS_SEIDEL)
     return fail(c, IE_ERR_INVALID_ARGUMENT, "solve_dd: unknown scheme");
   const int M = o->n_boxes;
   if (M < 1 || !o->boxes) return fail(c, IE_ERR_INVALID_ARGUMENT, "solve_dd: no boxes");
@@ -555,6 +558,204 @@ ie_status ie_solve_dd(ie_ctx* c, const ie_dd_opts* o, void* e_dev, int32_t init_
   for (int i = 0; i < M; ++i) {
     const ie_box& b = o->boxes[i];
     groups[{b.i1 - b.i0, b.j1 - b.j0, b.k1 - b.k0, c->layered ? b.k0 : 0}].push_back(i);
+  }
+
+  // ------------------------------------------------ Krylov-accelerated DD
+  // Flexible GMRES(kFgmresRestart) on the full system (I - G dsigma) E = E0, right-
+  // preconditioned by one DD sweep from zero (block Jacobi: z_i = A_ii^-1 v_i, batched;
+  // block Gauss-Seidel: z_i = A_ii^-1 (v_i + sum_{j<i} (G dsigma z_j)|_i)) with inner GMRES to the
+  // fixed tolerance inner_tol_fixed.  The preconditioner changes between applications, hence
+  // FGMRES (Saad 1993): the solution update uses the stored preconditioned vectors Z.
+  if (o->scheme == IE_DD_FGMRES_JACOBI || o->scheme == IE_DD_FGMRES_GAUSS_SEIDEL) {
+    const bool jac = o->scheme == IE_DD_FGMRES_JACOBI;
+    const int mo = kFgmresRestart;
+    double2* Vb = (double2*)ar.take((size_t)(mo + 1) * len * sizeof(double2));
+    double2* Zb = (double2*)ar.take((size_t)mo * len * sizeof(double2));
+    if (!Vb || !Zb) return fail(c, IE_ERR_OUT_OF_MEMORY, "workspace too small for the outer FGMRES basis");
+    auto Vj = [&](int j) { return Vb + (long long)j * len; };
+    auto Zj = [&](int j) { return Zb + (long long)j * len; };
+    const double thr = o->inner_tol_fixed;
+    // z = M^-1 v for right-hand side r (box buffers of rhs r)
+    auto precond_apply = [&](const double2* v, double2* z, int r) -> ie_status {
+      std::vector<int> rr1{r};
+      if (jac) {
+        for (auto& g : groups) {
+          for (int i : g.second) {
+            launch_gather(c, v, Bb + boff[i] + r * nbox(i), o->boxes[i], 1, 0, 0);
+            launch_axpby(c, Xb + boff[i] + r * nbox(i), 0.0, Bb + boff[i] + r * nbox(i), 0.0, nullptr, nbox(i));
+          }
+          std::vector<GmresSystem> sys;
+          for (int i : g.second)
+            sys.push_back(make_sys(c, Bb + boff[i] + r * nbox(i), Xb + boff[i] + r * nbox(i), o->boxes[i], thr,
+                                   std::max(1, o->inner.min_iters), o->inner.precond));
+          const ie_box& b0 = o->boxes[g.second[0]];
+          std::vector<GmresResult> res;
+          const size_t mark = ar.used;
+          long long ap = 0;
+          ie_status s2 = gmres_batched(c, ar, b0.i1 - b0.i0, b0.j1 - b0.j0, b0.k1 - b0.k0, b0.k0,
+                                       (long long)c->g.nx * c->g.ny, c->g.nx, sys, m, o->inner.max_iters, res, &ap);
+          ar.used = mark;
+          if (s2) return s2;
+          stats->sub_applies += (int)ap;
+          for (auto& q : res) {
+            stats->total_inner_iters += q.iters;
+            if (q.breakdown) breakdown = true;
+          }
+        }
+        for (int i = 0; i < M; ++i) launch_scatter(c, z, Xb + boff[i] + r * nbox(i), o->boxes[i], 1, 0, 0);
+        return IE_OK;
+      }
+      double2* Sr = S + r * len;
+      double2* Tr = T + r * len;
+      launch_axpby(c, Sr, 0.0, v, 0.0, nullptr, len);
+      launch_axpby(c, z, 0.0, v, 0.0, nullptr, len);
+      for (int i = 0; i < M; ++i) {
+        launch_axpby(c, Tr, 1.0, v, 1.0, Sr, len);  // v + sum_{j<i} G dsigma z_j
+        double2* bb = Bb + boff[i] + r * nbox(i);
+        double2* xb = Xb + boff[i] + r * nbox(i);
+        launch_gather(c, Tr, bb, o->boxes[i], 1, 0, 0);
+        launch_axpby(c, xb, 0.0, bb, 0.0, nullptr, nbox(i));
+        std::vector<GmresSystem> sys{make_sys(c, bb, xb, o->boxes[i], thr, std::max(1, o->inner.min_iters),
+                                              o->inner.precond)};
+        const ie_box& b0 = o->boxes[i];
+        std::vector<GmresResult> res;
+        const size_t mark = ar.used;
+        long long ap = 0;
+        ie_status s2 = gmres_batched(c, ar, b0.i1 - b0.i0, b0.j1 - b0.j0, b0.k1 - b0.k0, b0.k0,
+                                     (long long)c->g.nx * c->g.ny, c->g.nx, sys, m, o->inner.max_iters, res, &ap);
+        ar.used = mark;
+        if (s2) return s2;
+        stats->sub_applies += (int)ap;
+        stats->total_inner_iters += res[0].iters;
+        if (res[0].breakdown) breakdown = true;
+        launch_scatter(c, z, xb, o->boxes[i], 1, 0, 0);
+        if (i + 1 < M) {
+          stats->full_applies += 1;
+          s2 = apply_many(c, ar, fb, o->boxes[i], {xb}, {Sr}, 0.0, 1.0, 1);
+          if (s2) return s2;
+        }
+      }
+      return IE_OK;
+    };
+    int outer = 0;
+    for (int r = 0; r < ns; ++r) {
+      if (!active[r]) continue;
+      double2* x = E + r * len;
+      const double bnorm = e0n[r];
+      bool done = false;
+      int it = 0;
+      while (!done && it < o->max_sweeps) {
+        // true residual r0 = E0 - A x into V_0
+        launch_axpby(c, Vj(0), 1.0, c->e0 + r * len, 0.0, nullptr, len);
+        stats->full_applies += 1;
+        st = apply_many(c, ar, fb, fb, {x}, {Vj(0)}, -1.0, 1.0, 1);
+        if (st) return st;
+        double b2;
+        st = norms2(c, Vj(0), nullptr, 1, len, 0, &b2);
+        if (st) return st;
+        const double beta = sqrt(b2);
+        e[r] = bnorm > 0 ? beta / bnorm : 0.0;
+        if (!std::isfinite(beta)) {
+          breakdown = true;
+          break;
+        }
+        if (e[r] <= o->outer_tol || beta == 0.0) {
+          done = true;  // e[r] is the true residual
+          break;
+        }
+        launch_axpby(c, Vj(0), 1.0 / beta, Vj(0), 0.0, nullptr, len);
+        std::vector<cplx> H((size_t)(mo + 1) * mo, 0.0), cs(mo), sn(mo), g(mo + 1, 0.0), y;
+        g[0] = beta;
+        int k = 0;
+        for (; k < mo && it < o->max_sweeps; ++k) {
+          st = precond_apply(Vj(k), Zj(k), r);
+          if (st) return st;
+          stats->full_applies += 1;
+          st = apply_many(c, ar, fb, fb, {Zj(k)}, {Vj(k + 1)}, 1.0, -1.0, 0);  // w = A z_k
+          if (st) return st;
+          std::vector<cplx> h(k + 1), h2(k + 1);
+          double w2, w2b;
+          st = vec_dots(c, ar, Vj(k + 1), Vb, k + 1, len, h.data(), &w2);
+          if (st) return st;
+          std::vector<cplx> neg(k + 1);
+          double hs = 0;
+          for (int j = 0; j <= k; ++j) {
+            neg[j] = -h[j];
+            hs += std::norm(h[j]);
+          }
+          st = vec_axpy(c, ar, Vj(k + 1), Vj(k + 1), Vb, k + 1, neg.data(), len);
+          if (st) return st;
+          if (w2 - hs < 0.01 * w2) {  // DGKS re-orthogonalisation (eta = 0.1, as the inner GMRES)
+            st = vec_dots(c, ar, Vj(k + 1), Vb, k + 1, len, h2.data(), &w2b);
+            if (st) return st;
+            for (int j = 0; j <= k; ++j) {
+              neg[j] = -h2[j];
+              h[j] += h2[j];
+            }
+            st = vec_axpy(c, ar, Vj(k + 1), Vj(k + 1), Vb, k + 1, neg.data(), len);
+            if (st) return st;
+          }
+          double nw2;
+          st = norms2(c, Vj(k + 1), nullptr, 1, len, 0, &nw2);
+          if (st) return st;
+          const double hk1 = sqrt(nw2);
+          cplx* Hk = &H[(size_t)k * (mo + 1)];
+          for (int j = 0; j <= k; ++j) Hk[j] = h[j];
+          Hk[k + 1] = hk1;
+          for (int j = 0; j < k; ++j) {
+            const cplx t = cs[j] * Hk[j] + sn[j] * Hk[j + 1];
+            Hk[j + 1] = -std::conj(sn[j]) * Hk[j] + std::conj(cs[j]) * Hk[j + 1];
+            Hk[j] = t;
+          }
+          const cplx a = Hk[k], bb = Hk[k + 1];
+          const double den = sqrt(std::norm(a) + std::norm(bb));
+          cs[k] = den == 0.0 ? cplx(1.0) : std::conj(a / den);
+          sn[k] = den == 0.0 ? cplx(0.0) : std::conj(bb / den);
+          Hk[k] = cs[k] * a + sn[k] * bb;
+          Hk[k + 1] = 0.0;
+          g[k + 1] = -std::conj(sn[k]) * g[k];
+          g[k] = cs[k] * g[k];
+          ++it;
+          ++outer;
+          const double est = std::abs(g[k + 1]) / bnorm;
+          if (stats->e_hist && outer <= o->max_sweeps) stats->e_hist[(size_t)outer * ns + r] = est;
+          if (hk1 > 0) launch_axpby(c, Vj(k + 1), 1.0 / hk1, Vj(k + 1), 0.0, nullptr, len);
+          if (est <= o->outer_tol || !(hk1 > 1e-14 * std::abs(Hk[k]))) {
+            ++k;
+            break;
+          }
+        }
+        // x += Z y, y = H^-1 g (upper triangular)
+        y.assign(k, 0.0);
+        for (int j = k - 1; j >= 0; --j) {
+          cplx t = g[j];
+          for (int l = j + 1; l < k; ++l) t -= H[(size_t)l * (mo + 1) + j] * y[l];
+          y[j] = t / H[(size_t)j * (mo + 1) + j];
+        }
+        st = vec_axpy(c, ar, x, x, Zb, k, y.data(), len);
+        if (st) return st;
+      }
+      if (!done) {  // final true residual
+        launch_axpby(c, T + r * len, 1.0, c->e0 + r * len, 0.0, nullptr, len);
+        stats->full_applies += 1;
+        st = apply_many(c, ar, fb, fb, {x}, {T + r * len}, -1.0, 1.0, 1);
+        if (st) return st;
+        double v2;
+        st = norms2(c, T + r * len, nullptr, 1, len, 0, &v2);
+        if (st) return st;
+        e[r] = bnorm > 0 ? sqrt(v2) / bnorm : 0.0;
+      }
+    }
+    IE_CUDA(c, cudaStreamSynchronize(c->stream));
+    stats->sweeps = outer;
+    bool allc = true;
+    for (int r = 0; r < ns; ++r) {
+      stats->e_final = std::max(stats->e_final, e[r]);
+      allc = allc && e[r] <= o->outer_tol;
+    }
+    if (breakdown) return fail(c, IE_ERR_BREAKDOWN, "non-finite values in the Krylov-accelerated DD");
+    if (!allc) return fail(c, IE_ERR_NOT_CONVERGED, "Krylov-accelerated DD reached max_sweeps outer iterations");
+    return IE_OK;
   }
 
   int sweep = 0;

@@ -202,5 +202,11 @@ ie_status gmres_batched(ie_ctx* c, Arena& ar, int nx, int ny, int nz, int k0, lo
                         const std::vector<GmresSystem>& sys, int restart, int max_iters,
                         std::vector<GmresResult>& res, long long* applies);
 size_t gmres_scratch_bytes(int nx, int ny, int nz, int nsys, int restart);
+// single full-length vectors (FGMRES outer basis): h_j = <V_j, w>, ||w||^2 (host results);
+// out = base + sum_j coef_j V_j
+ie_status vec_dots(ie_ctx* c, Arena& ar, const double2* w, const double2* V, int nv, long long len, cplx* h,
+                   double* wn2);
+ie_status vec_axpy(ie_ctx* c, Arena& ar, double2* out, const double2* base, const double2* V, int nv,
+                   const cplx* coef, long long len);
 
 }  // namespace ie

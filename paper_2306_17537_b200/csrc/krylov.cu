@@ -527,4 +527,58 @@ ie_status gmres_batched(ie_ctx* c, Arena& ar, int nx, int ny, int nz, int k0, lo
   return IE_OK;
 }
 
+// --------------------------------------------------------------- single-vector helpers
+// (the FGMRES outer iteration of the Krylov-accelerated DD, api.cu)
+ie_status vec_dots(ie_ctx* c, Arena& ar, const double2* w, const double2* V, int nv, long long len, cplx* h,
+                   double* wn2) {
+  const int nblk = dot_blocks(1);
+  const size_t mark = ar.used;
+  DotJob* dj = (DotJob*)ar.take(sizeof(DotJob));
+  double2* part = (double2*)ar.take((size_t)(nv + 1) * nblk * sizeof(double2));
+  double2* rows = (double2*)ar.take((size_t)(nv + 1) * sizeof(double2));
+  if (!dj || !part || !rows) {
+    ar.used = mark;
+    return fail(c, IE_ERR_OUT_OF_MEMORY, "workspace too small for the outer Krylov basis");
+  }
+  const DotJob hj{w, V, nv, 0};
+  IE_CUDA(c, cudaMemcpyAsync(dj, &hj, sizeof(DotJob), cudaMemcpyHostToDevice, c->stream));
+  k_mdot<kDotG><<<dim3(nblk, nv / kDotG + 1, 1), 256, 0, c->stream>>>(dj, len, part, nblk);
+  IE_CHECK_LAUNCH(c, "k_mdot");
+  k_reduce_rows<<<nv + 1, 128, 0, c->stream>>>(part, nblk, rows);
+  IE_CHECK_LAUNCH(c, "k_reduce_rows");
+  std::vector<double2> hr(nv + 1);
+  IE_CUDA(c, cudaMemcpyAsync(hr.data(), rows, (nv + 1) * sizeof(double2), cudaMemcpyDeviceToHost, c->stream));
+  IE_CUDA(c, cudaStreamSynchronize(c->stream));
+  ar.used = mark;
+  for (int j = 0; j < nv; ++j) h[j] = cplx(hr[j].x, hr[j].y);
+  *wn2 = hr[nv].x;
+  return IE_OK;
+}
+
+ie_status vec_axpy(ie_ctx* c, Arena& ar, double2* out, const double2* base, const double2* V, int nv,
+                   const cplx* coef, long long len) {
+  if (nv == 0) {
+    if (out != base) launch_axpby(c, out, 1.0, base, 0.0, nullptr, len);
+    return IE_OK;
+  }
+  const size_t mark = ar.used;
+  AxpyJob* aj = (AxpyJob*)ar.take(sizeof(AxpyJob));
+  double2* cf = (double2*)ar.take((size_t)nv * sizeof(double2));
+  if (!aj || !cf) {
+    ar.used = mark;
+    return fail(c, IE_ERR_OUT_OF_MEMORY, "workspace too small for the outer Krylov basis");
+  }
+  const AxpyJob hj{out, base, V, nv, 0};
+  std::vector<double2> hc(nv);
+  for (int j = 0; j < nv; ++j) hc[j] = make_double2(coef[j].real(), coef[j].imag());
+  IE_CUDA(c, cudaMemcpyAsync(aj, &hj, sizeof(AxpyJob), cudaMemcpyHostToDevice, c->stream));
+  IE_CUDA(c, cudaMemcpyAsync(cf, hc.data(), nv * sizeof(double2), cudaMemcpyHostToDevice, c->stream));
+  const int gx = (int)std::max<long long>(1, std::min<long long>((len + 255) / 256, 1184));
+  k_maxpy<<<dim3(gx, 1), 256, 0, c->stream>>>(aj, cf, len);
+  IE_CHECK_LAUNCH(c, "k_maxpy");
+  IE_CUDA(c, cudaStreamSynchronize(c->stream));  // the staging is released below
+  ar.used = mark;
+  return IE_OK;
+}
+
 }  // namespace ie

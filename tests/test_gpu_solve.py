@@ -196,3 +196,34 @@ def test_c2mod_preconditioned_matches_oracle_gmres(scheme):
     e = _field(cfg, 1)
     st = ie.ie_solve_dd(ctx, e, scheme, boxes=cfg.boxes, outer_tol=1e-9, restart=30, max_sweeps=300, precond=1)
     assert rel(e.cpu().numpy()[0], Xref) < FIELD_TOL
+
+
+@pytest.mark.parametrize("name", ["c2mini", "c3mini", "c5mini"])
+@pytest.mark.parametrize("scheme", ["fgmres_jacobi", "fgmres_gauss_seidel"])
+@pytest.mark.parametrize("precond", [0, 1])
+def test_krylov_accelerated_dd_matches_dense_lu(name, scheme, precond):
+    """FGMRES right-preconditioned by one block-Jacobi / block-GS sweep
+    reaches the dense LU solution."""
+    import paper_2306_17537_b200 as ie
+    cfg = make_config(name)
+    ctx, sigma = gpu_ctx(cfg)
+    k0, ds, E0, X = _lu_truth(cfg, sigma)
+    e = _field(cfg, len(cfg.sources))
+    st = ie.ie_solve_dd(ctx, e, scheme, boxes=cfg.boxes, outer_tol=1e-9, restart=cfg.restart,
+                        inner_tol_fixed=1e-2, max_sweeps=100, precond=precond)
+    assert st["e_final"] <= 1e-9
+    assert rel(e.cpu().numpy(), X) < FIELD_TOL
+
+
+@pytest.mark.parametrize("scheme", ["fgmres_jacobi", "fgmres_gauss_seidel"])
+def test_c2mod_krylov_dd_matches_oracle_gmres(scheme):
+    import paper_2306_17537_b200 as ie
+    cfg = make_config("c2mod")
+    ctx, sigma = gpu_ctx(cfg)
+    k0, ds, E0 = oracle_setup(cfg, sigma)
+    Aop = op.Operator(cfg.n, cfg.hvec, k0, cfg.sigma_b, ds)
+    Xref, info = gmres(Aop, E0[0], x0=E0[0], tol=1e-12, restart=30, max_iters=3000)
+    e = _field(cfg, 1)
+    st = ie.ie_solve_dd(ctx, e, scheme, boxes=cfg.boxes, outer_tol=1e-9, restart=30, inner_tol_fixed=1e-2,
+                        max_sweeps=100)
+    assert rel(e.cpu().numpy()[0], Xref) < FIELD_TOL
