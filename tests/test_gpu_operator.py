@@ -28,7 +28,9 @@ def _cfg(n, h=0.2, sigma_b=0.3, freq=4e5):
 SHAPES = [(8, 8, 8), (16, 8, 4), (4, 16, 32), (1, 2, 4), (2, 1, 1), (32, 4, 2), (64, 8, 16), (8, 64, 2),
           (2, 2, 128), (128, 2, 2), (512, 1, 2),
           # radix-16 z-pass variants (L, W) = (64, 8|16|32), (128, 8|16), (256, 8)
-          (4, 8, 32), (8, 4, 32), (32, 4, 32), (4, 4, 64), (16, 4, 64), (8, 2, 128)]
+          (4, 8, 32), (8, 4, 32), (32, 4, 32), (4, 4, 64), (16, 4, 64), (8, 2, 128),
+          # maximum and large generic FFT lengths (2n = 1024 / 512 on z, the generic z-pass)
+          (2, 2, 512), (4, 8, 256), (1, 1, 1)]
 
 
 @pytest.mark.parametrize("n", SHAPES)
