@@ -458,7 +458,7 @@ __global__ void __launch_bounds__(512) k_yinv(const __grid_constant__ ApplyParam
 // One component per CTA row group (blockIdx.y = item*3 + component): the inverse x-FFT and
 // the identity update never mix components, so a thread holds one line (8 values) and the
 // kernel runs at high occupancy.
-template <int L>
+template <int L, bool PRE>
 __global__ void __launch_bounds__(128) k_xinv(const __grid_constant__ ApplyParams p) {
   using P = FftPlan<L>;
   constexpr int T = P::T, V = P::V, R0 = P::radix(0, false), RL = P::radix(P::NST - 1, false);
@@ -490,7 +490,7 @@ __global__ void __launch_bounds__(128) k_xinv(const __grid_constant__ ApplyParam
   const double2* xrow = it.x + l * N + off;
   // contraction-IE right preconditioner: the identity term is (P x)_l (row l of sym6 P)
   const int pc0 = l == 0 ? 0 : (l == 1 ? 3 : 4), pc1 = l == 0 ? 3 : (l == 1 ? 1 : 5), pc2 = l == 0 ? 4 : (l == 1 ? 5 : 2);
-  const double* prow = it.pm ? it.pm + zz * p.ds_zs + yy * p.ds_ys : nullptr;
+  const double* prow = PRE ? it.pm + zz * p.ds_zs + yy * p.ds_ys : nullptr;
   const double2* x0row = it.x + off;
 #pragma unroll
   for (int u = 0; u < V / RL; ++u)
@@ -500,7 +500,7 @@ __global__ void __launch_bounds__(128) k_xinv(const __grid_constant__ ApplyParam
       double2 o = cscale(v[0][u * RL + r], b);
       if (a != 0.0) {
         double2 xi;
-        if (prow) {
+        if constexpr (PRE) {
           const double q0 = __ldg(prow + pc0 * p.ds_cs + x), q1 = __ldg(prow + pc1 * p.ds_cs + x),
                        q2 = __ldg(prow + pc2 * p.ds_cs + x);
           const double2 e0 = ld2(x0row + x), e1 = ld2(x0row + N + x), e2 = ld2(x0row + 2 * N + x);
@@ -687,14 +687,19 @@ static cudaError_t go_yinv(const ApplyParams& p, cudaStream_t s) {
   k_yinv<L><<<dim3(p.x2w / W, p.nz, 3 * p.n_items), W * T, smem, s>>>(p);
   return cudaGetLastError();
 }
-template <int L>
-static cudaError_t go_xinv(const ApplyParams& p, cudaStream_t s) {
+template <int L, bool PRE>
+static cudaError_t go_xinv_p(const ApplyParams& p, cudaStream_t s) {
   const int T = FftPlan<L>::T, rows = rows_per_cta(T);
   const size_t smem = (size_t)rows * padded(L) * sizeof(double2);
-  cudaError_t e = prep((const void*)k_xinv<L>, smem);
+  cudaError_t e = prep((const void*)k_xinv<L, PRE>, smem);
   if (e) return e;
-  k_xinv<L><<<dim3((p.ny * p.nz + rows - 1) / rows, 3 * p.n_items), rows * T, smem, s>>>(p);
+  k_xinv<L, PRE><<<dim3((p.ny * p.nz + rows - 1) / rows, 3 * p.n_items), rows * T, smem, s>>>(p);
   return cudaGetLastError();
+}
+template <int L>
+static cudaError_t go_xinv(const ApplyParams& p, cudaStream_t s) {
+  // items of one launch are either all preconditioned (contraction IE) or none
+  return p.items[0].pm ? go_xinv_p<L, true>(p, s) : go_xinv_p<L, false>(p, s);
 }
 
 template <int L> static void wrap_xfwd(cudaError_t* e, const ApplyParams& p, cudaStream_t s, int m) { *e = go_xfwd<L>(p, s, m); }
