@@ -31,7 +31,7 @@ __device__ __forceinline__ double2 ld2_stream(const double2* p) {
 
 // =====================================================================  K-A
 template <int L>
-__global__ void __launch_bounds__(128, 4) k_xfwd(const __grid_constant__ ApplyParams p) {
+__global__ void __launch_bounds__(128, 5) k_xfwd(const __grid_constant__ ApplyParams p) {
   using P = FftPlan<L>;
   constexpr int T = P::T, V = P::V, R0 = P::radix(0, false), RL = P::radix(P::NST - 1, false);
   extern __shared__ double2 sm[];
