@@ -394,7 +394,8 @@ def run_ours(args, cfg, sigma, rank, ws, local):
     dom = max(shares, key=shares.get)
     achieved = kb[dom] / (shares[dom] / 1e3) / 1e9
     kernels = {k: {"ms": round(shares[k], 4), "share": round(shares[k] / sum(shares.values()), 4),
-                   "alg_bytes": kb[k], "gbs": round(kb[k] / (shares[k] / 1e3) / 1e9, 1)} for k in shares}
+                   "alg_bytes": kb[k], "gbs": round(kb[k] / (shares[k] / 1e3) / 1e9, 1),
+                   "frac_of_hbm_peak": round(kb[k] / (shares[k] / 1e3) / 1e9 / peak, 3)} for k in shares}
 
     # --- e2e through the public API with HOST buffers (pinned), copies inside the timed region:
     # every step copies its input host->device and reads its result back device->host; the copies
