@@ -12,6 +12,7 @@
 #include <math.h>
 
 #include <algorithm>
+#include <mutex>
 #include <unordered_map>
 #include <vector>
 
@@ -586,9 +587,12 @@ static int threads_per_line() {
 }
 
 // opt in to > 48 KB dynamic shared memory (once per kernel instance and size)
+// (separate contexts may be driven from different host threads: the cache is locked)
 static cudaError_t prep(const void* kernel, size_t smem) {
   static std::unordered_map<const void*, size_t> done;
+  static std::mutex mu;
   if (smem <= 48 * 1024) return cudaSuccess;
+  std::lock_guard<std::mutex> lock(mu);
   auto f = done.find(kernel);
   if (f != done.end() && f->second >= smem) return cudaSuccess;
   cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
