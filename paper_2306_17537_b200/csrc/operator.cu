@@ -10,6 +10,7 @@
 // The 1/(8 nx ny nz) normalisation is folded into the packed spectrum (green.cu).
 // See DESIGN.md §Kernels for the traffic model (1344 N + 96 (nx+1)(ny+1)(nz+1) bytes).
 #include <math.h>
+#include <stdlib.h>
 
 #include <algorithm>
 #include <mutex>
@@ -677,7 +678,9 @@ static cudaError_t go_zconv16_w(const ApplyParams& p, cudaStream_t s) {
 static cudaError_t go_zconv16(const ApplyParams& p, cudaStream_t s, int W) {
   const int L = 2 * p.nz;
   if (L == 256) return go_zconv16_w<256, 8>(p, s);
-  if (L == 128) return W == 16 ? go_zconv16_w<128, 16>(p, s) : go_zconv16_w<128, 8>(p, s);
+  // 8-pencil tiles (128-byte rows): more, smaller CTAs per SM measured faster than 128-thread
+  // tiles for L = 128 (c4h K-C 0.212 -> 0.202 ms)
+  if (L == 128) return go_zconv16_w<128, 8>(p, s);
   if (L == 64)
     return W == 32 ? go_zconv16_w<64, 32>(p, s) : (W == 16 ? go_zconv16_w<64, 16>(p, s) : go_zconv16_w<64, 8>(p, s));
   return cudaErrorInvalidValue;
