@@ -429,6 +429,186 @@ __global__ void __launch_bounds__(128, 2) k_zconv16(const __grid_constant__ Appl
   }
 }
 
+// K-C, tensor-memory variant for L = 256 (W = 8 pencils, T = 16 threads per pencil).  The
+// forward z-FFT leaves thread t holding kz = t + 16 r (r < 16) of its pencil; the spectra of
+// components 0 and 1 are parked in the thread's own TMEM lane (128 columns), component 2 stays in
+// registers, the 3x3 multiply runs thread-locally, and the inverse starts from those registers --
+// no shared-memory round trip for the parked spectra or the multiply (half the shared-memory
+// wavefronts of k_zconv16).  Shared memory holds the staged inputs (z < nz, 3 components) plus one
+// spare block, reused as the exchange buffers of the radix-16 stages: 68 KB, 3 CTAs per SM.
+// Threads t and 16 - t (mirror partners: kz and L - kz use the same octant Green plane) sit in
+// the same warp so the duplicated Green loads hit L1.
+template <int LA>
+__global__ void __launch_bounds__(128, 3) k_zconv16t(const __grid_constant__ ApplyParams p) {
+  constexpr int L = 256, W = 8, T = 16, NZ = 128;
+  constexpr uint32_t kCols = 128;
+  extern __shared__ __align__(16) double2 sm[];
+  double2* twl = sm + 4 * NZ * W;  // exp(-2 pi i m / L), m < L
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(twl + L);
+  const int c = threadIdx.x % W, q = threadIdx.x / W;
+  const int t = (q & 1) ? (q == 1 ? 8 : 16 - (q >> 1)) : (q >> 1);  // warp w: {t, 16 - t} pairs
+  const ApplyItem& it = p.items[blockIdx.z];
+  const int nx = p.nx, ny = p.ny, Lx = 2 * nx, Ly = 2 * ny, Xw = p.x2w;
+  const int kx0 = p.k0x + blockIdx.x * W, kx = kx0 + c;
+  const int by = blockIdx.y;
+  const int ky = (by == 0) ? 0 : (by == 1 ? ny : ((by & 1) ? Ly - (by >> 1) : (by >> 1)));
+  const long long cs = (long long)NZ * Ly * Xw, zs = (long long)Ly * Xw;
+  double2* tile = p.X2 + (long long)blockIdx.z * 3 * cs + (long long)ky * Xw + (kx0 - p.k0x);
+  const long long gcs = (long long)(NZ + 1) * (ny + 1) * (nx + 1);
+  const long long gzs = (long long)(ny + 1) * (nx + 1);
+  const int ix = kx <= nx ? kx : Lx - kx;
+  const int iy = ky <= ny ? ky : Ly - ky;
+  const double2* g = p.ghat + (long long)iy * (nx + 1) + ix;
+
+  if (threadIdx.x < 32) tmem_alloc(tslot, kCols);
+  {
+    const int z0 = it.sz0, z1 = it.sz1;
+#pragma unroll
+    for (int l = 0; l < 3; ++l)
+      for (int z = t; z < NZ; z += T) {
+        double2* d = &sm[(l * NZ + z) * W + c];
+        if (z >= z0 && z < z1) cp_async16(d, tile + l * cs + z * zs + c);
+        else *d = czero();
+      }
+    for (int m = threadIdx.x; m < L; m += blockDim.x) cp_async16(&twl[m], &p.pw_z[m]);
+    const int ixmin = (kx0 + W - 1 <= nx) ? kx0 : Lx - kx0 - (W - 1);
+    const double2* g0 = p.ghat + (long long)iy * (nx + 1) + ixmin;
+    for (int qq = threadIdx.x; qq < 6 * (NZ + 1); qq += blockDim.x) {
+      const double2* row = g0 + (qq / (NZ + 1)) * gcs + (qq % (NZ + 1)) * gzs;
+      prefetch_l2(row);
+      prefetch_l2(row + (W - 1));
+    }
+    cp_async_wait_all();
+    tmem_fence_before();
+    __syncthreads();
+    tmem_fence_after();
+  }
+  const uint32_t taddr = *tslot + ((uint32_t)(32 * (threadIdx.x / 32)) << 16);
+
+  // exchange rows of component l's forward pass: rows < NZ in its own staging block, the rest in
+  // the spare block
+  auto xrow = [&](int l, int row) -> double2* {
+    return row < NZ ? sm + (l * NZ + row) * W + c : sm + (3 * NZ + row - NZ) * W + c;
+  };
+  auto forward = [&](int l, double2(&v)[16]) {
+#pragma unroll
+    for (int r = 0; r < 8; ++r) v[r] = sm[(l * NZ + t + r * T) * W + c];  // z = t + 16 r < nz
+    dft16<-1, true>(v);
+    __syncthreads();  // every input row of component l read before the exchange overwrites it
+#pragma unroll
+    for (int r = 0; r < 16; ++r) *xrow(l, t * 16 + r) = v[r];
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+      double2 x = *xrow(l, t + 16 * r);
+      if (r > 0) x = cmul(x, twl[r * t]);
+      v[r] = x;
+    }
+    dft16<-1>(v);  // v[r] = spectrum at kz = t + 16 r
+  };
+  auto tm_put16 = [&](uint32_t col, const double2(&v)[16]) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) tmem_st4(taddr + col + 16 * i, &v[4 * i]);
+  };
+  auto tm_get16 = [&](uint32_t col, double2(&v)[16]) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) tmem_ld4(taddr + col + 16 * i, &v[4 * i]);
+  };
+
+  // multiply order: i -> r = i/2 (even i) or 15 - i/2 (odd i), so mirror partners' loads of the
+  // same Green plane issue back to back
+  auto r_of = [](int i) { return (i & 1) ? 15 - (i >> 1) : (i >> 1); };
+  auto load_g = [&](int r, double2(&G)[6]) {
+    const int kz = t + 16 * r, iz = kz <= NZ ? kz : L - kz;
+#pragma unroll
+    for (int k = 0; k < 6; ++k) G[k] = ld2(g + iz * gzs + k * gcs);
+  };
+  const unsigned fx = kx > nx ? 0x80000000u : 0u, fy = ky > ny ? 0x80000000u : 0u;
+
+  double2 v[16];
+#pragma unroll 1
+  for (int l = 0; l < 2; ++l) {  // one copy of the code (instruction-cache footprint)
+    forward(l, v);
+    tm_put16(64 * l, v);
+  }
+  tmem_wait_st();
+  double2 Gq[LA][6];  // Green values of the next LA multiply steps, in flight
+#pragma unroll
+  for (int a = 0; a < LA; ++a) load_g(r_of(a), Gq[a]);
+  forward(2, v);
+#pragma unroll
+  for (int s = 0; s < 8; ++s) {  // two kz per step (i = 2s, 2s+1)
+    uint32_t raw[16];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int r = r_of(2 * s + h);
+      tmem_ld4_raw(taddr + 4 * r, raw + 8 * h);
+      tmem_ld4_raw(taddr + 64 + 4 * r, raw + 8 * h + 4);
+    }
+    tmem_wait_ld16(raw);
+    double2 J[2][2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      J[h][0] = raw_to_z(raw + 8 * h);
+      J[h][1] = raw_to_z(raw + 8 * h + 4);
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int i = 2 * s + h, r = r_of(i);
+      double2 G[6];
+#pragma unroll
+      for (int k = 0; k < 6; ++k) G[k] = Gq[i % LA][k];
+      if (i + LA < 16) load_g(r_of(i + LA), Gq[i % LA]);
+      const int kz = t + 16 * r;
+      const unsigned fz = kz > NZ ? 0x80000000u : 0u;
+      const double2 gxy = flip_if(G[3], fx ^ fy), gxz = flip_if(G[4], fx ^ fz), gyz = flip_if(G[5], fy ^ fz);
+      const double2 j0 = J[h][0], j1 = J[h][1], j2 = v[r];
+      J[h][0] = cdot3(G[0], j0, gxy, j1, gxz, j2);
+      J[h][1] = cdot3(gxy, j0, G[1], j1, gyz, j2);
+      v[r] = cdot3(gxz, j0, gyz, j1, G[2], j2);
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int r = r_of(2 * s + h);
+      tmem_st1(taddr + 4 * r, J[h][0]);
+      tmem_st1(taddr + 64 + 4 * r, J[h][1]);
+    }
+  }
+  tmem_wait_st();
+
+  // inverse z-FFT from registers: radix 16 over r, exchange, twiddle + radix 16, crop, store
+  auto inverse = [&](int l, double2(&v)[16], double2* B) {
+    dft16<+1>(v);
+#pragma unroll
+    for (int r = 0; r < 16; ++r) B[(t * 16 + r) * W + c] = v[r];
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+      double2 x = B[(t + r * T) * W + c];
+      if (r > 0) x = cmulc(x, twl[r * t]);  // exp(+2 pi i r t / L)
+      v[r] = x;
+    }
+    dft16<+1, false, true>(v);
+    double2* dst = tile + l * cs + c;
+#pragma unroll
+    for (int r = 0; r < 8; ++r) dst[(long long)(t + r * T) * zs] = v[r];  // z = t + 16 r < nz
+  };
+  // buffers: component 2 -> staging blocks 0-1, component 0 -> block 2 + spare, component 1 ->
+  // blocks 0-1 again (one barrier per component separates each reuse)
+  inverse(2, v, sm);
+#pragma unroll 1
+  for (int l = 0; l < 2; ++l) {
+    tm_get16(64 * l, v);
+    inverse(l, v, l == 0 ? sm + 2 * NZ * W : sm);
+  }
+  tmem_fence_before();
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    tmem_fence_after();
+    tmem_dealloc(*tslot, kCols);
+  }
+}
+
 // =====================================================================  K-D
 template <int L>
 __global__ void __launch_bounds__(512) k_yinv(const __grid_constant__ ApplyParams p) {
@@ -675,9 +855,28 @@ static cudaError_t go_zconv16_w(const ApplyParams& p, cudaStream_t s) {
   k_zconv16<L, W><<<dim3(p.x2w / W, 2 * p.ny, p.n_items), W * (L / 16), smem, s>>>(p);
   return cudaGetLastError();
 }
+template <int LA>
+static cudaError_t go_zconv16t(const ApplyParams& p, cudaStream_t s) {
+  const size_t smem = (size_t)(4 * 128 * 8 + 256 + 1) * sizeof(double2);
+  cudaError_t e = prep((const void*)k_zconv16t<LA>, smem);
+  if (e) return e;
+  k_zconv16t<LA><<<dim3(p.x2w / 8, 2 * p.ny, p.n_items), 128, smem, s>>>(p);
+  return cudaGetLastError();
+}
 static cudaError_t go_zconv16(const ApplyParams& p, cudaStream_t s, int W) {
   const int L = 2 * p.nz;
-  if (L == 256) return go_zconv16_w<256, 8>(p, s);
+  if (L == 256) {
+    // IE_KC_VARIANT: 0 = shared-memory-parked spectra (k_zconv16), 1/2/3 = TMEM-parked with
+    // that many multiply steps of Green loads in flight (2: c5 K-C 1.79 -> 1.69 ms)
+    static const int kc = [] {
+      const char* e = getenv("IE_KC_VARIANT");
+      return e ? atoi(e) : 2;
+    }();
+    if (kc == 1) return go_zconv16t<1>(p, s);
+    if (kc == 2) return go_zconv16t<2>(p, s);
+    if (kc == 3) return go_zconv16t<3>(p, s);
+    return go_zconv16_w<256, 8>(p, s);
+  }
   // 8-pencil tiles (128-byte rows): more, smaller CTAs per SM measured faster than 128-thread
   // tiles for L = 128 (c4h K-C 0.212 -> 0.202 ms)
   if (L == 128) return go_zconv16_w<128, 8>(p, s);

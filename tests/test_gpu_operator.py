@@ -155,3 +155,17 @@ def test_config_operator_matches_oracle_fft(name):
     yh = y.cpu().numpy()
     for r in range(len(cfg.sources)):
         assert rel(yh[r], A(E0[r])) < TOL
+
+
+@pytest.mark.parametrize("variant", ["0", "1", "3"])
+def test_zpass_variants_match_oracle(variant):
+    """The non-default L = 256 z-pass kernels (IE_KC_VARIANT; read once per process, hence the
+    subprocess) pass the same operator parity as the default."""
+    import os
+    import subprocess
+    import sys
+    env = dict(os.environ, IE_KC_VARIANT=variant)
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider",
+                        os.path.abspath(__file__) + "::test_apply_operator_matches_oracle"],
+                       env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
