@@ -438,7 +438,9 @@ __global__ void __launch_bounds__(128, 2) k_zconv16(const __grid_constant__ Appl
 // spare block, reused as the exchange buffers of the radix-16 stages: 68 KB, 3 CTAs per SM.
 // Threads t and 16 - t (mirror partners: kz and L - kz use the same octant Green plane) sit in
 // the same warp so the duplicated Green loads hit L1.
-template <int LA>
+// GS: the Green planes are staged into shared memory (cp.async, 4 chunks of 33 octant planes,
+// ping-pong between the two halves freed by the forward passes) instead of register lookahead
+template <int LA, bool GS = false>
 __global__ void __launch_bounds__(128, 3) k_zconv16t(const __grid_constant__ ApplyParams p) {
   constexpr int L = 256, W = 8, T = 16, NZ = 128;
   constexpr uint32_t kCols = 128;
@@ -490,11 +492,24 @@ __global__ void __launch_bounds__(128, 3) k_zconv16t(const __grid_constant__ App
   auto xrow = [&](int l, int row) -> double2* {
     return row < NZ ? sm + (l * NZ + row) * W + c : sm + (3 * NZ + row - NZ) * W + c;
   };
+  // Green chunk k: octant planes iz in [32k, 32k + 32], layout [6][33][W], own column only
+  constexpr int GR = 33;
+  auto g_chunk = [&](int k, double2* R) {
+    for (int row = t; row < GR; row += T) {
+      const double2* src = g + (32 * k + row) * gzs;
+#pragma unroll
+      for (int comp = 0; comp < 6; ++comp) cp_async16(R + (comp * GR + row) * W + c, src + comp * gcs);
+    }
+    cp_async_commit();
+  };
+  double2* const RA = sm;               // staging blocks 0-1
+  double2* const RB = sm + 2 * NZ * W;  // staging block 2 + spare
   auto forward = [&](int l, double2(&v)[16]) {
 #pragma unroll
     for (int r = 0; r < 8; ++r) v[r] = sm[(l * NZ + t + r * T) * W + c];  // z = t + 16 r < nz
     dft16<-1, true>(v);
     __syncthreads();  // every input row of component l read before the exchange overwrites it
+    if (GS && l == 2) g_chunk(0, RA);  // blocks 0-1 are free once component 1 is done
 #pragma unroll
     for (int r = 0; r < 16; ++r) *xrow(l, t * 16 + r) = v[r];
     __syncthreads();
@@ -532,6 +547,45 @@ __global__ void __launch_bounds__(128, 3) k_zconv16t(const __grid_constant__ App
     tm_put16(64 * l, v);
   }
   tmem_wait_st();
+  if constexpr (GS) {
+    forward(2, v);
+    __syncthreads();  // block 2 + spare read
+    g_chunk(1, RB);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if (k == 0) cp_async_wait<1>();
+      else cp_async_wait<0>();
+      __syncthreads();  // chunk k landed (all threads' copies); chunk k-1 fully consumed
+      if (k == 1) g_chunk(2, RA);
+      if (k == 2) g_chunk(3, RB);
+      const double2* R = (k & 1) ? RB : RA;
+#pragma unroll
+      for (int s = 2 * k; s < 2 * k + 2; ++s) {
+        uint32_t raw[16];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int r = r_of(2 * s + h);
+          tmem_ld4_raw(taddr + 4 * r, raw + 8 * h);
+          tmem_ld4_raw(taddr + 64 + 4 * r, raw + 8 * h + 4);
+        }
+        tmem_wait_ld16(raw);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int r = r_of(2 * s + h), kz = t + 16 * r, iz = kz <= NZ ? kz : L - kz;
+          const double2* gr = R + (iz - 32 * k) * W + c;
+          double2 G[6];
+#pragma unroll
+          for (int q6 = 0; q6 < 6; ++q6) G[q6] = gr[q6 * GR * W];
+          const unsigned fz = kz > NZ ? 0x80000000u : 0u;
+          const double2 gxy = flip_if(G[3], fx ^ fy), gxz = flip_if(G[4], fx ^ fz), gyz = flip_if(G[5], fy ^ fz);
+          const double2 j0 = raw_to_z(raw + 8 * h), j1 = raw_to_z(raw + 8 * h + 4), j2 = v[r];
+          tmem_st1(taddr + 4 * r, cdot3(G[0], j0, gxy, j1, gxz, j2));
+          tmem_st1(taddr + 64 + 4 * r, cdot3(gxy, j0, G[1], j1, gyz, j2));
+          v[r] = cdot3(gxz, j0, gyz, j1, G[2], j2);
+        }
+      }
+    }
+  } else {
   double2 Gq[LA][6];  // Green values of the next LA multiply steps, in flight
 #pragma unroll
   for (int a = 0; a < LA; ++a) load_g(r_of(a), Gq[a]);
@@ -573,6 +627,7 @@ __global__ void __launch_bounds__(128, 3) k_zconv16t(const __grid_constant__ App
       tmem_st1(taddr + 4 * r, J[h][0]);
       tmem_st1(taddr + 64 + 4 * r, J[h][1]);
     }
+  }
   }
   tmem_wait_st();
 
@@ -855,26 +910,28 @@ static cudaError_t go_zconv16_w(const ApplyParams& p, cudaStream_t s) {
   k_zconv16<L, W><<<dim3(p.x2w / W, 2 * p.ny, p.n_items), W * (L / 16), smem, s>>>(p);
   return cudaGetLastError();
 }
-template <int LA>
+template <int LA, bool GS = false>
 static cudaError_t go_zconv16t(const ApplyParams& p, cudaStream_t s) {
   const size_t smem = (size_t)(4 * 128 * 8 + 256 + 1) * sizeof(double2);
-  cudaError_t e = prep((const void*)k_zconv16t<LA>, smem);
+  cudaError_t e = prep((const void*)k_zconv16t<LA, GS>, smem);
   if (e) return e;
-  k_zconv16t<LA><<<dim3(p.x2w / 8, 2 * p.ny, p.n_items), 128, smem, s>>>(p);
+  k_zconv16t<LA, GS><<<dim3(p.x2w / 8, 2 * p.ny, p.n_items), 128, smem, s>>>(p);
   return cudaGetLastError();
 }
 static cudaError_t go_zconv16(const ApplyParams& p, cudaStream_t s, int W) {
   const int L = 2 * p.nz;
   if (L == 256) {
     // IE_KC_VARIANT: 0 = shared-memory-parked spectra (k_zconv16), 1/2/3 = TMEM-parked with
-    // that many multiply steps of Green loads in flight (2: c5 K-C 1.79 -> 1.69 ms)
+    // that many multiply steps of Green loads in flight (2: c5 K-C 1.79 -> 1.69 ms), 4 = TMEM-
+    // parked with the Green planes staged through shared memory (1.52 ms)
     static const int kc = [] {
       const char* e = getenv("IE_KC_VARIANT");
-      return e ? atoi(e) : 2;
+      return e ? atoi(e) : 4;
     }();
     if (kc == 1) return go_zconv16t<1>(p, s);
     if (kc == 2) return go_zconv16t<2>(p, s);
     if (kc == 3) return go_zconv16t<3>(p, s);
+    if (kc == 4) return go_zconv16t<1, true>(p, s);
     return go_zconv16_w<256, 8>(p, s);
   }
   // 8-pencil tiles (128-byte rows): more, smaller CTAs per SM measured faster than 128-thread
