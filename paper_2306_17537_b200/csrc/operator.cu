@@ -475,11 +475,14 @@ __global__ void __launch_bounds__(128, 3) k_zconv16t(const __grid_constant__ App
     for (int m = threadIdx.x; m < L; m += blockDim.x) cp_async16(&twl[m], &p.pw_z[m]);
     const int ixmin = (kx0 + W - 1 <= nx) ? kx0 : Lx - kx0 - (W - 1);
     const double2* g0 = p.ghat + (long long)iy * (nx + 1) + ixmin;
-    for (int qq = threadIdx.x; qq < 6 * (NZ + 1); qq += blockDim.x) {
-      const double2* row = g0 + (qq / (NZ + 1)) * gcs + (qq % (NZ + 1)) * gzs;
-      prefetch_l2(row);
-      prefetch_l2(row + (W - 1));
-    }
+    // component-major: consecutive threads take consecutive planes of one component
+#pragma unroll
+    for (int comp = 0; comp < 6; ++comp)
+      for (int iz = threadIdx.x; iz <= NZ; iz += blockDim.x) {
+        const double2* row = g0 + comp * gcs + iz * gzs;
+        prefetch_l2(row);
+        prefetch_l2(row + (W - 1));
+      }
     cp_async_wait_all();
     tmem_fence_before();
     __syncthreads();
@@ -559,19 +562,21 @@ __global__ void __launch_bounds__(128, 3) k_zconv16t(const __grid_constant__ App
       if (k == 1) g_chunk(2, RA);
       if (k == 2) g_chunk(3, RB);
       const double2* R = (k & 1) ? RB : RA;
+      constexpr int KPW = LA == 2 ? 1 : 2;  // kz per TMEM wait (GS: LA picks 1 or 2)
 #pragma unroll
-      for (int s = 2 * k; s < 2 * k + 2; ++s) {
-        uint32_t raw[16];
+      for (int i0 = 4 * k; i0 < 4 * k + 4; i0 += KPW) {
+        uint32_t raw[8 * KPW];
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int r = r_of(2 * s + h);
+        for (int h = 0; h < KPW; ++h) {
+          const int r = r_of(i0 + h);
           tmem_ld4_raw(taddr + 4 * r, raw + 8 * h);
           tmem_ld4_raw(taddr + 64 + 4 * r, raw + 8 * h + 4);
         }
-        tmem_wait_ld16(raw);
+        if constexpr (KPW == 1) tmem_wait_ld8(raw);
+        else tmem_wait_ld16(raw);
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int r = r_of(2 * s + h), kz = t + 16 * r, iz = kz <= NZ ? kz : L - kz;
+        for (int h = 0; h < KPW; ++h) {
+          const int r = r_of(i0 + h), kz = t + 16 * r, iz = kz <= NZ ? kz : L - kz;
           const double2* gr = R + (iz - 32 * k) * W + c;
           double2 G[6];
 #pragma unroll
@@ -932,6 +937,7 @@ static cudaError_t go_zconv16(const ApplyParams& p, cudaStream_t s, int W) {
     if (kc == 2) return go_zconv16t<2>(p, s);
     if (kc == 3) return go_zconv16t<3>(p, s);
     if (kc == 4) return go_zconv16t<1, true>(p, s);
+    if (kc == 5) return go_zconv16t<2, true>(p, s);
     return go_zconv16_w<256, 8>(p, s);
   }
   // 8-pencil tiles (128-byte rows): more, smaller CTAs per SM measured faster than 128-thread
@@ -1150,6 +1156,11 @@ ie_status launch_apply(ie_ctx* c, ApplyParams& p) {
   p.pw_z = c->tw.powers(2 * p.nz);
   p.x2w = 2 * p.nx;
   p.k0x = 0;
+  static const int knob = [] {
+    const char* e = getenv("IE_KNOB");
+    return e ? atoi(e) : 0;
+  }();
+  p.knob = knob;
   const int S = c->slabs ? slab_width(p) : 0;  // off unless IE_SLABS=1 (measured slower)
   cudaError_t e = S ? run_apply_slabs(c, p, c->stream, S) : run_apply(c, p, c->stream);
   if (e != cudaSuccess) return cuda_fail(c, e, "operator kernels");
