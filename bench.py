@@ -390,7 +390,7 @@ def run_ours(args, cfg, sigma, rank, ws, local):
 
     # roofline of the dominant kernel (largest share of the step)
     kb = kernel_bytes(nx, ny, nz)
-    shares = {k: v[0] / max(1, v[1]) for k, v in prof.items()}
+    shares = {k: v[0] / max(1, v[1]) for k, v in prof.items() if v[1] > 0 and v[0] > 0}
     dom = max(shares, key=shares.get)
     achieved = kb[dom] / (shares[dom] / 1e3) / 1e9
     kernels = {k: {"ms": round(shares[k], 4), "share": round(shares[k] / sum(shares.values()), 4),
