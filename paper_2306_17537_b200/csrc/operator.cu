@@ -13,6 +13,7 @@
 #include <stdlib.h>
 
 #include <algorithm>
+#include <type_traits>
 #include <mutex>
 #include <unordered_map>
 #include <vector>
@@ -440,7 +441,9 @@ __global__ void __launch_bounds__(128, 2) k_zconv16(const __grid_constant__ Appl
 // the same warp so the duplicated Green loads hit L1.
 // GS: the Green planes are staged into shared memory (cp.async, 4 chunks of 33 octant planes,
 // ping-pong between the two halves freed by the forward passes) instead of register lookahead
-template <int LA, bool GS = false>
+// TW: stage twiddles w^(r t) as products w^(4a t) w^(b t) of 6 loaded powers (9 complex
+// multiplies) instead of 15 shared loads
+template <int LA, bool GS = false, int TW = 0>
 __global__ void __launch_bounds__(128, 3) k_zconv16t(const __grid_constant__ ApplyParams p) {
   constexpr int L = 256, W = 8, T = 16, NZ = 128;
   constexpr uint32_t kCols = 128;
@@ -507,6 +510,37 @@ __global__ void __launch_bounds__(128, 3) k_zconv16t(const __grid_constant__ App
   };
   double2* const RA = sm;               // staging blocks 0-1
   double2* const RB = sm + 2 * NZ * W;  // staging block 2 + spare
+  // v[r] *= w^(r t) (CONJ: conj) for r = 1..15
+  auto twiddle = [&](double2(&v)[16], auto conj_tag) {
+    constexpr bool CONJ = decltype(conj_tag)::value;
+    if constexpr (TW == 2) {  // 2 loads, 4 more multiplies
+      const double2 b1 = twl[t], a1 = twl[4 * t];
+      const double2 b2 = cmul(b1, b1), a2 = cmul(a1, a1);
+      const double2 b3 = cmul(b2, b1), a3 = cmul(a2, a1);
+      const double2 bb[4] = {make_double2(1.0, 0.0), b1, b2, b3};
+      const double2 aa[4] = {make_double2(1.0, 0.0), a1, a2, a3};
+#pragma unroll
+      for (int r = 1; r < 16; ++r) {
+        const int a = r >> 2, b = r & 3;
+        const double2 w = (a == 0) ? bb[b] : (b == 0 ? aa[a] : cmul(aa[a], bb[b]));
+        v[r] = CONJ ? cmulc(v[r], w) : cmul(v[r], w);
+      }
+    } else if constexpr (TW == 1) {
+      const double2 b1 = twl[t], b2 = twl[2 * t], b3 = twl[3 * t];
+      const double2 a1 = twl[4 * t], a2 = twl[8 * t], a3 = twl[12 * t];
+      const double2 bb[4] = {make_double2(1.0, 0.0), b1, b2, b3};
+      const double2 aa[4] = {make_double2(1.0, 0.0), a1, a2, a3};
+#pragma unroll
+      for (int r = 1; r < 16; ++r) {
+        const int a = r >> 2, b = r & 3;
+        const double2 w = (a == 0) ? bb[b] : (b == 0 ? aa[a] : cmul(aa[a], bb[b]));
+        v[r] = CONJ ? cmulc(v[r], w) : cmul(v[r], w);
+      }
+    } else {
+#pragma unroll
+      for (int r = 1; r < 16; ++r) v[r] = CONJ ? cmulc(v[r], twl[r * t]) : cmul(v[r], twl[r * t]);
+    }
+  };
   auto forward = [&](int l, double2(&v)[16]) {
 #pragma unroll
     for (int r = 0; r < 8; ++r) v[r] = sm[(l * NZ + t + r * T) * W + c];  // z = t + 16 r < nz
@@ -517,11 +551,8 @@ __global__ void __launch_bounds__(128, 3) k_zconv16t(const __grid_constant__ App
     for (int r = 0; r < 16; ++r) *xrow(l, t * 16 + r) = v[r];
     __syncthreads();
 #pragma unroll
-    for (int r = 0; r < 16; ++r) {
-      double2 x = *xrow(l, t + 16 * r);
-      if (r > 0) x = cmul(x, twl[r * t]);
-      v[r] = x;
-    }
+    for (int r = 0; r < 16; ++r) v[r] = *xrow(l, t + 16 * r);
+    twiddle(v, std::false_type{});
     dft16<-1>(v);  // v[r] = spectrum at kz = t + 16 r
   };
   auto tm_put16 = [&](uint32_t col, const double2(&v)[16]) {
@@ -643,11 +674,8 @@ __global__ void __launch_bounds__(128, 3) k_zconv16t(const __grid_constant__ App
     for (int r = 0; r < 16; ++r) B[(t * 16 + r) * W + c] = v[r];
     __syncthreads();
 #pragma unroll
-    for (int r = 0; r < 16; ++r) {
-      double2 x = B[(t + r * T) * W + c];
-      if (r > 0) x = cmulc(x, twl[r * t]);  // exp(+2 pi i r t / L)
-      v[r] = x;
-    }
+    for (int r = 0; r < 16; ++r) v[r] = B[(t + r * T) * W + c];
+    twiddle(v, std::true_type{});  // exp(+2 pi i r t / L)
     dft16<+1, false, true>(v);
     double2* dst = tile + l * cs + c;
 #pragma unroll
@@ -915,29 +943,32 @@ static cudaError_t go_zconv16_w(const ApplyParams& p, cudaStream_t s) {
   k_zconv16<L, W><<<dim3(p.x2w / W, 2 * p.ny, p.n_items), W * (L / 16), smem, s>>>(p);
   return cudaGetLastError();
 }
-template <int LA, bool GS = false>
+template <int LA, bool GS = false, int TW = 0>
 static cudaError_t go_zconv16t(const ApplyParams& p, cudaStream_t s) {
   const size_t smem = (size_t)(4 * 128 * 8 + 256 + 1) * sizeof(double2);
-  cudaError_t e = prep((const void*)k_zconv16t<LA, GS>, smem);
+  cudaError_t e = prep((const void*)k_zconv16t<LA, GS, TW>, smem);
   if (e) return e;
-  k_zconv16t<LA, GS><<<dim3(p.x2w / 8, 2 * p.ny, p.n_items), 128, smem, s>>>(p);
+  k_zconv16t<LA, GS, TW><<<dim3(p.x2w / 8, 2 * p.ny, p.n_items), 128, smem, s>>>(p);
   return cudaGetLastError();
 }
 static cudaError_t go_zconv16(const ApplyParams& p, cudaStream_t s, int W) {
   const int L = 2 * p.nz;
   if (L == 256) {
     // IE_KC_VARIANT: 0 = shared-memory-parked spectra (k_zconv16), 1/2/3 = TMEM-parked with
-    // that many multiply steps of Green loads in flight (2: c5 K-C 1.79 -> 1.69 ms), 4 = TMEM-
-    // parked with the Green planes staged through shared memory (1.52 ms)
+    // that many multiply steps of Green loads in flight (2: c5 K-C 1.79 -> 1.69 ms), 4/5 = TMEM-
+    // parked with the Green planes staged through shared memory (1.53 ms), 6/7 = 4 with the
+    // stage twiddles as products of 6 / 2 loaded powers (1.47 / 1.46 ms, the default)
     static const int kc = [] {
       const char* e = getenv("IE_KC_VARIANT");
-      return e ? atoi(e) : 4;
+      return e ? atoi(e) : 7;
     }();
     if (kc == 1) return go_zconv16t<1>(p, s);
     if (kc == 2) return go_zconv16t<2>(p, s);
     if (kc == 3) return go_zconv16t<3>(p, s);
     if (kc == 4) return go_zconv16t<1, true>(p, s);
     if (kc == 5) return go_zconv16t<2, true>(p, s);
+    if (kc == 6) return go_zconv16t<1, true, 1>(p, s);
+    if (kc == 7) return go_zconv16t<1, true, 2>(p, s);
     return go_zconv16_w<256, 8>(p, s);
   }
   // 8-pencil tiles (128-byte rows): more, smaller CTAs per SM measured faster than 128-thread

@@ -157,7 +157,7 @@ def test_config_operator_matches_oracle_fft(name):
         assert rel(yh[r], A(E0[r])) < TOL
 
 
-@pytest.mark.parametrize("variant", ["0", "1", "2", "3", "5"])
+@pytest.mark.parametrize("variant", ["0", "1", "2", "3", "4", "5", "6"])
 def test_zpass_variants_match_oracle(variant):
     """The non-default L = 256 z-pass kernels (IE_KC_VARIANT; read once per process, hence the
     subprocess) pass the same operator parity as the default."""
