@@ -269,13 +269,17 @@ __global__ void __launch_bounds__(128, 2) k_zconv16(const __grid_constant__ Appl
   extern __shared__ __align__(16) double2 sm[];
   double2* twl = sm + 3 * L * W;  // exp(-2 pi i m / L), m < L
   const int c = threadIdx.x % W, t = threadIdx.x / W;
-  const ApplyItem& it = p.items[blockIdx.z];
+  // items fastest in launch order: the CTAs of one pencil tile for all right-hand sides run
+  // together and share its Green rows through L2
+  const int item = p.n_items == 1 ? 0 : blockIdx.x % p.n_items;
+  const int xt = p.n_items == 1 ? blockIdx.x : blockIdx.x / p.n_items;
+  const ApplyItem& it = p.items[item];
   const int nx = p.nx, ny = p.ny, Lx = 2 * nx, Ly = 2 * ny, Xw = p.x2w;
-  const int kx0 = p.k0x + blockIdx.x * W, kx = kx0 + c;
+  const int kx0 = p.k0x + xt * W, kx = kx0 + c;
   const int by = blockIdx.y;  // mirror pairs (ky, 2ny-ky) adjacent in launch order (L2 reuse of G)
   const int ky = (by == 0) ? 0 : (by == 1 ? ny : ((by & 1) ? Ly - (by >> 1) : (by >> 1)));
   const long long cs = (long long)NZ * Ly * Xw, zs = (long long)Ly * Xw;
-  double2* tile = p.X2 + (long long)blockIdx.z * 3 * cs + (long long)ky * Xw + (kx0 - p.k0x);
+  double2* tile = p.X2 + (long long)item * 3 * cs + (long long)ky * Xw + (kx0 - p.k0x);
   const long long gcs = (long long)(NZ + 1) * (ny + 1) * (nx + 1);
   const long long gzs = (long long)(ny + 1) * (nx + 1);
   const int ix = kx <= nx ? kx : Lx - kx;
@@ -452,13 +456,17 @@ __global__ void __launch_bounds__(128, 3) k_zconv16t(const __grid_constant__ App
   uint32_t* tslot = reinterpret_cast<uint32_t*>(twl + L);
   const int c = threadIdx.x % W, q = threadIdx.x / W;
   const int t = (q & 1) ? (q == 1 ? 8 : 16 - (q >> 1)) : (q >> 1);  // warp w: {t, 16 - t} pairs
-  const ApplyItem& it = p.items[blockIdx.z];
+  // items fastest in launch order: the CTAs of one pencil tile for all right-hand sides run
+  // together and share its Green rows through L2
+  const int item = p.n_items == 1 ? 0 : blockIdx.x % p.n_items;
+  const int xt = p.n_items == 1 ? blockIdx.x : blockIdx.x / p.n_items;
+  const ApplyItem& it = p.items[item];
   const int nx = p.nx, ny = p.ny, Lx = 2 * nx, Ly = 2 * ny, Xw = p.x2w;
-  const int kx0 = p.k0x + blockIdx.x * W, kx = kx0 + c;
+  const int kx0 = p.k0x + xt * W, kx = kx0 + c;
   const int by = blockIdx.y;
   const int ky = (by == 0) ? 0 : (by == 1 ? ny : ((by & 1) ? Ly - (by >> 1) : (by >> 1)));
   const long long cs = (long long)NZ * Ly * Xw, zs = (long long)Ly * Xw;
-  double2* tile = p.X2 + (long long)blockIdx.z * 3 * cs + (long long)ky * Xw + (kx0 - p.k0x);
+  double2* tile = p.X2 + (long long)item * 3 * cs + (long long)ky * Xw + (kx0 - p.k0x);
   const long long gcs = (long long)(NZ + 1) * (ny + 1) * (nx + 1);
   const long long gzs = (long long)(ny + 1) * (nx + 1);
   const int ix = kx <= nx ? kx : Lx - kx;
@@ -940,7 +948,7 @@ static cudaError_t go_zconv16_w(const ApplyParams& p, cudaStream_t s) {
   const size_t smem = (size_t)(3 * L * W + L) * sizeof(double2);
   cudaError_t e = prep((const void*)k_zconv16<L, W>, smem);
   if (e) return e;
-  k_zconv16<L, W><<<dim3(p.x2w / W, 2 * p.ny, p.n_items), W * (L / 16), smem, s>>>(p);
+  k_zconv16<L, W><<<dim3(p.n_items * (p.x2w / W), 2 * p.ny), W * (L / 16), smem, s>>>(p);
   return cudaGetLastError();
 }
 template <int LA, bool GS = false, int TW = 0>
@@ -948,7 +956,7 @@ static cudaError_t go_zconv16t(const ApplyParams& p, cudaStream_t s) {
   const size_t smem = (size_t)(4 * 128 * 8 + 256 + 1) * sizeof(double2);
   cudaError_t e = prep((const void*)k_zconv16t<LA, GS, TW>, smem);
   if (e) return e;
-  k_zconv16t<LA, GS, TW><<<dim3(p.x2w / 8, 2 * p.ny, p.n_items), 128, smem, s>>>(p);
+  k_zconv16t<LA, GS, TW><<<dim3(p.n_items * (p.x2w / 8), 2 * p.ny), 128, smem, s>>>(p);
   return cudaGetLastError();
 }
 static cudaError_t go_zconv16(const ApplyParams& p, cudaStream_t s, int W) {
