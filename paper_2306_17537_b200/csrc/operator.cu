@@ -705,6 +705,205 @@ __global__ void __launch_bounds__(128, 3) k_zconv16t(const __grid_constant__ App
   }
 }
 
+// K-C, TMEM-parked z-pass for L = 2nz in {128, 256} (the design of k_zconv16t<1, true, 2>,
+// generalised): T = L/16 threads per pencil, W = 2048/L pencils per CTA (128 threads, one TMEM
+// lane each).  Forward: radix 16 (first stage, half the inputs zero) then U = 16/R1 radix-R1
+// stages per thread (R1 = L/16), after which thread t holds kz = j + 16 r for j = t + u T
+// (u < U, r < R1): 16 values per component.  Components 0, 1 are parked in the thread's TMEM lane,
+// component 2 stays in registers, the 3x3 multiply is thread-local with the Green planes staged
+// through shared memory in 4 chunks of NZ/4 + 1 octant planes (chunk k serves the r whose octant
+// plane iz = min(kz, L - kz) falls in it, for every u), and the inverse starts from registers.
+// Stage twiddles w^(r j) = w^(4a j) w^(b j) (r = 4a + b) from two loaded powers.  Threads of
+// mirror-partner pencil positions (t, T - t) share a warp.
+template <int L>
+__global__ void __launch_bounds__(128, 3) k_zconv_tm(const __grid_constant__ ApplyParams p) {
+  constexpr int NZ = L / 2, T = L / 16, W = 2048 / L, R1 = L / 16, U = 16 / R1;
+  constexpr int CH = NZ / 4, GR = CH + 1;  // Green chunk: planes [CH k, CH k + CH]
+  static_assert(L == 128 || L == 256, "TMEM z-pass: L in {128, 256}");
+  static_assert(W * T == 128 && U * R1 == 16, "one TMEM lane per thread, 16 values per component");
+  static_assert(6 * GR * W <= 2 * NZ * W, "a Green chunk fits one half of the staging area");
+  constexpr uint32_t kCols = 128;
+  extern __shared__ __align__(16) double2 sm[];
+  double2* twl = sm + 4 * NZ * W;  // exp(-2 pi i m / L), m < L
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(twl + L);
+  const int c = threadIdx.x % W, q = threadIdx.x / W;
+  // pencil position t of lane group q, with t and its mirror partner T - t in one warp
+  int t;
+  if constexpr (L == 256) t = (q & 1) ? (q == 1 ? 8 : 16 - (q >> 1)) : (q >> 1);
+  else t = (int)((0x53627140u >> (4 * q)) & 7);  // q -> {0, 4, 1, 7, 2, 6, 3, 5}
+  const int item = p.n_items == 1 ? 0 : blockIdx.x % p.n_items;
+  const int xt = p.n_items == 1 ? blockIdx.x : blockIdx.x / p.n_items;
+  const ApplyItem& it = p.items[item];
+  const int nx = p.nx, ny = p.ny, Lx = 2 * nx, Ly = 2 * ny, Xw = p.x2w;
+  const int kx0 = p.k0x + xt * W, kx = kx0 + c;
+  const int by = blockIdx.y;
+  const int ky = (by == 0) ? 0 : (by == 1 ? ny : ((by & 1) ? Ly - (by >> 1) : (by >> 1)));
+  const long long cs = (long long)NZ * Ly * Xw, zs = (long long)Ly * Xw;
+  double2* tile = p.X2 + (long long)item * 3 * cs + (long long)ky * Xw + (kx0 - p.k0x);
+  const long long gcs = (long long)(NZ + 1) * (ny + 1) * (nx + 1);
+  const long long gzs = (long long)(ny + 1) * (nx + 1);
+  const int ix = kx <= nx ? kx : Lx - kx;
+  const int iy = ky <= ny ? ky : Ly - ky;
+  const double2* g = p.ghat + (long long)iy * (nx + 1) + ix;
+
+  if (threadIdx.x < 32) tmem_alloc(tslot, kCols);
+  {
+    const int z0 = it.sz0, z1 = it.sz1;
+#pragma unroll
+    for (int l = 0; l < 3; ++l)
+      for (int z = q; z < NZ; z += T) {
+        double2* d = &sm[(l * NZ + z) * W + c];
+        if (z >= z0 && z < z1) cp_async16(d, tile + l * cs + z * zs + c);
+        else *d = czero();
+      }
+    for (int m = threadIdx.x; m < L; m += blockDim.x) cp_async16(&twl[m], &p.pw_z[m]);
+    const int ixmin = (kx0 + W - 1 <= nx) ? kx0 : Lx - kx0 - (W - 1);
+    const double2* g0 = p.ghat + (long long)iy * (nx + 1) + ixmin;
+#pragma unroll
+    for (int comp = 0; comp < 6; ++comp)
+      for (int iz = threadIdx.x; iz <= NZ; iz += blockDim.x) {
+        const double2* row = g0 + comp * gcs + iz * gzs;
+#pragma unroll
+        for (int o = 0; o < W; o += 8) prefetch_l2(row + o);
+        prefetch_l2(row + (W - 1));
+      }
+    cp_async_wait_all();
+    tmem_fence_before();
+    __syncthreads();
+    tmem_fence_after();
+  }
+  const uint32_t taddr = *tslot + ((uint32_t)(32 * (threadIdx.x / 32)) << 16);
+
+  auto xrow = [&](int l, int row) -> double2* {
+    return row < NZ ? sm + (l * NZ + row) * W + c : sm + (3 * NZ + row - NZ) * W + c;
+  };
+  auto g_chunk = [&](int k, double2* R) {
+    for (int row = q; row < GR; row += T) {
+      const double2* src = g + (CH * k + row) * gzs;
+#pragma unroll
+      for (int comp = 0; comp < 6; ++comp) cp_async16(R + (comp * GR + row) * W + c, src + comp * gcs);
+    }
+    cp_async_commit();
+  };
+  double2* const RA = sm;               // staging blocks 0-1
+  double2* const RB = sm + 2 * NZ * W;  // staging block 2 + spare
+  // v[r] *= w^(r j) (CONJ: conj) for r = 1 .. n-1, from w^j and w^(4j)
+  auto twiddle = [&](double2* v, int n, int j, auto conj_tag) {
+    constexpr bool CONJ = decltype(conj_tag)::value;
+    const double2 b1 = twl[j], a1 = twl[4 * j];
+    const double2 b2 = cmul(b1, b1), b3 = cmul(b2, b1);
+    const double2 a2 = cmul(a1, a1), a3 = cmul(a2, a1);
+    const double2 bb[4] = {make_double2(1.0, 0.0), b1, b2, b3};
+    const double2 aa[4] = {make_double2(1.0, 0.0), a1, a2, a3};
+#pragma unroll
+    for (int r = 1; r < 16; ++r) {
+      if (r >= n) break;
+      const int a = r >> 2, b = r & 3;
+      const double2 w = (a == 0) ? bb[b] : (b == 0 ? aa[a] : cmul(aa[a], bb[b]));
+      v[r] = CONJ ? cmulc(v[r], w) : cmul(v[r], w);
+    }
+  };
+  auto forward = [&](int l, double2(&v)[16], bool hook) {
+#pragma unroll
+    for (int r = 0; r < 8; ++r) v[r] = sm[(l * NZ + t + r * T) * W + c];  // z = t + r T < nz
+    dft16<-1, true>(v);
+    __syncthreads();  // every input row of component l read before the exchange overwrites it
+    if (hook) g_chunk(0, RA);  // blocks 0-1 are free once component 1 is done
+#pragma unroll
+    for (int r = 0; r < 16; ++r) *xrow(l, t * 16 + r) = v[r];
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int j = t + u * T;
+#pragma unroll
+      for (int r = 0; r < R1; ++r) v[u * R1 + r] = *xrow(l, j + 16 * r);
+      twiddle(&v[u * R1], R1, j, std::false_type{});
+      dftR<R1, -1>(&v[u * R1]);  // v[u R1 + r] = spectrum at kz = j + 16 r
+    }
+  };
+  const unsigned fx = kx > nx ? 0x80000000u : 0u, fy = ky > ny ? 0x80000000u : 0u;
+  // chunk serving stage-2 index r: iz = kz = j + 16 r (r < R1/2) or L - kz (r >= R1/2)
+  auto chunk_of = [](int r) { return r < R1 / 2 ? (16 * r) / CH : (16 * (R1 - 1 - r)) / CH; };
+
+  double2 v[16];
+#pragma unroll 1
+  for (int l = 0; l < 2; ++l) {
+    forward(l, v, false);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) tmem_st4(taddr + 64 * l + 16 * i, &v[4 * i]);
+  }
+  tmem_wait_st();
+  forward(2, v, true);
+  __syncthreads();  // block 2 + spare read
+  g_chunk(1, RB);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    if (k == 0) cp_async_wait<1>();
+    else cp_async_wait<0>();
+    __syncthreads();  // chunk k landed (all threads' copies); chunk k-1 fully consumed
+    if (k == 1) g_chunk(2, RA);
+    if (k == 2) g_chunk(3, RB);
+    const double2* R = (k & 1) ? RB : RA;
+#pragma unroll
+    for (int r = 0; r < R1; ++r) {
+      if (chunk_of(r) != k) continue;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int s = u * R1 + r;  // slot of kz = j + 16 r
+        uint32_t raw[8];
+        tmem_ld4_raw(taddr + 4 * s, raw);
+        tmem_ld4_raw(taddr + 64 + 4 * s, raw + 4);
+        tmem_wait_ld8(raw);
+        const int kz = t + u * T + 16 * r, iz = kz <= NZ ? kz : L - kz;
+        const double2* gr = R + (iz - CH * k) * W + c;
+        double2 G[6];
+#pragma unroll
+        for (int q6 = 0; q6 < 6; ++q6) G[q6] = gr[q6 * GR * W];
+        const unsigned fz = kz > NZ ? 0x80000000u : 0u;
+        const double2 gxy = flip_if(G[3], fx ^ fy), gxz = flip_if(G[4], fx ^ fz), gyz = flip_if(G[5], fy ^ fz);
+        const double2 j0 = raw_to_z(raw), j1 = raw_to_z(raw + 4), j2 = v[s];
+        tmem_st1(taddr + 4 * s, cdot3(G[0], j0, gxy, j1, gxz, j2));
+        tmem_st1(taddr + 64 + 4 * s, cdot3(gxy, j0, G[1], j1, gyz, j2));
+        v[s] = cdot3(gxz, j0, gyz, j1, G[2], j2);
+      }
+    }
+  }
+  tmem_wait_st();
+
+  // inverse z-FFT from registers: radix R1 per j, exchange, twiddle + radix 16, crop, store
+  auto inverse = [&](int l, double2(&v)[16], double2* B) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) dftR<R1, +1>(&v[u * R1]);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int j = t + u * T;
+#pragma unroll
+      for (int r = 0; r < R1; ++r) B[(j * R1 + r) * W + c] = v[u * R1 + r];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < 16; ++r) v[r] = B[(t + r * T) * W + c];
+    twiddle(v, 16, t, std::true_type{});  // exp(+2 pi i r t / L)
+    dft16<+1, false, true>(v);
+    double2* dst = tile + l * cs + c;
+#pragma unroll
+    for (int r = 0; r < 8; ++r) dst[(long long)(t + r * T) * zs] = v[r];  // z = t + r T < nz
+  };
+  inverse(2, v, sm);
+#pragma unroll 1
+  for (int l = 0; l < 2; ++l) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) tmem_ld4(taddr + 64 * l + 16 * i, &v[4 * i]);
+    inverse(l, v, l == 0 ? sm + 2 * NZ * W : sm);
+  }
+  tmem_fence_before();
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    tmem_fence_after();
+    tmem_dealloc(*tslot, kCols);
+  }
+}
+
 // =====================================================================  K-D
 template <int L>
 __global__ void __launch_bounds__(512) k_yinv(const __grid_constant__ ApplyParams p) {
@@ -959,6 +1158,15 @@ static cudaError_t go_zconv16t(const ApplyParams& p, cudaStream_t s) {
   k_zconv16t<LA, GS, TW><<<dim3(p.n_items * (p.x2w / 8), 2 * p.ny), 128, smem, s>>>(p);
   return cudaGetLastError();
 }
+template <int L>
+static cudaError_t go_zconv_tm(const ApplyParams& p, cudaStream_t s) {
+  constexpr int W = 2048 / L;
+  const size_t smem = (size_t)(4 * (L / 2) * W + L + 1) * sizeof(double2);
+  cudaError_t e = prep((const void*)k_zconv_tm<L>, smem);
+  if (e) return e;
+  k_zconv_tm<L><<<dim3(p.n_items * (p.x2w / W), 2 * p.ny), 128, smem, s>>>(p);
+  return cudaGetLastError();
+}
 static cudaError_t go_zconv16(const ApplyParams& p, cudaStream_t s, int W) {
   const int L = 2 * p.nz;
   if (L == 256) {
@@ -977,11 +1185,21 @@ static cudaError_t go_zconv16(const ApplyParams& p, cudaStream_t s, int W) {
     if (kc == 5) return go_zconv16t<2, true>(p, s);
     if (kc == 6) return go_zconv16t<1, true, 1>(p, s);
     if (kc == 7) return go_zconv16t<1, true, 2>(p, s);
+    if (kc == 8) return go_zconv_tm<256>(p, s);
     return go_zconv16_w<256, 8>(p, s);
   }
   // 8-pencil tiles (128-byte rows): more, smaller CTAs per SM measured faster than 128-thread
   // tiles for L = 128 (c4h K-C 0.212 -> 0.202 ms)
-  if (L == 128) return go_zconv16_w<128, 8>(p, s);
+  if (L == 128) {
+    // IE_KC128_VARIANT: 1 = TMEM-parked spectra (k_zconv_tm<128>, c4h apply 0.396 -> 0.366 ms,
+    // the default when the tile width divides 2nx), 0 = k_zconv16<128, 8>
+    static const int kc128 = [] {
+      const char* e = getenv("IE_KC128_VARIANT");
+      return e ? atoi(e) : 1;
+    }();
+    if (kc128 == 1 && (p.x2w % 16) == 0) return go_zconv_tm<128>(p, s);
+    return go_zconv16_w<128, 8>(p, s);
+  }
   if (L == 64)
     return W == 32 ? go_zconv16_w<64, 32>(p, s) : (W == 16 ? go_zconv16_w<64, 16>(p, s) : go_zconv16_w<64, 8>(p, s));
   return cudaErrorInvalidValue;

@@ -157,15 +157,17 @@ def test_config_operator_matches_oracle_fft(name):
         assert rel(yh[r], A(E0[r])) < TOL
 
 
-@pytest.mark.parametrize("variant", ["0", "1", "2", "3", "4", "5", "6"])
-def test_zpass_variants_match_oracle(variant):
-    """The non-default L = 256 z-pass kernels (IE_KC_VARIANT; read once per process, hence the
-    subprocess) pass the same operator parity as the default."""
+@pytest.mark.parametrize("env", ["IE_KC_VARIANT=0", "IE_KC_VARIANT=1", "IE_KC_VARIANT=2", "IE_KC_VARIANT=3",
+                                 "IE_KC_VARIANT=4", "IE_KC_VARIANT=5", "IE_KC_VARIANT=6", "IE_KC_VARIANT=7",
+                                 "IE_KC_VARIANT=8", "IE_KC128_VARIANT=0"])
+def test_zpass_variants_match_oracle(env):
+    """The non-default z-pass kernels (IE_KC_VARIANT for L = 256, IE_KC128_VARIANT for L = 128;
+    read once per process, hence the subprocess) pass the same operator parity as the default."""
     import os
     import subprocess
     import sys
-    env = dict(os.environ, IE_KC_VARIANT=variant)
+    k, v = env.split("=")
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider",
                         os.path.abspath(__file__) + "::test_apply_operator_matches_oracle"],
-                       env=env, capture_output=True, text=True, timeout=900)
+                       env=dict(os.environ, **{k: v}), capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
