@@ -213,9 +213,25 @@ __device__ __forceinline__ void fft_stage(double2 (&v)[NL][FftPlan<L>::V], doubl
   for (int u = 0; u < U; ++u) {
     const int j = t + u * T;
     const int k = j & (Ns - 1);
+    // stage twiddles w^r, w = exp(-2 pi i k / (Ns R)): R = 8 from two loaded powers (w, w^4)
+    // and five complex multiplies instead of seven loads; R = 4 from w alone
     double2 w[R];
+    if constexpr (R == 8) {
+      w[1] = __ldg(&tws[k]);
+      w[4] = __ldg(&tws[3 * Ns + k]);
+      w[2] = cmul(w[1], w[1]);
+      w[3] = cmul(w[2], w[1]);
+      w[5] = cmul(w[4], w[1]);
+      w[6] = cmul(w[4], w[2]);
+      w[7] = cmul(w[4], w[3]);
+    } else if constexpr (R == 4) {
+      w[1] = __ldg(&tws[k]);
+      w[2] = cmul(w[1], w[1]);
+      w[3] = cmul(w[2], w[1]);
+    } else {
 #pragma unroll
-    for (int r = 1; r < R; ++r) w[r] = __ldg(&tws[(r - 1) * Ns + k]);
+      for (int r = 1; r < R; ++r) w[r] = __ldg(&tws[(r - 1) * Ns + k]);
+    }
 #pragma unroll
     for (int l = 0; l < NL; ++l) {
 #pragma unroll

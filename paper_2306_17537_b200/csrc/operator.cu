@@ -906,7 +906,7 @@ __global__ void __launch_bounds__(128, 3) k_zconv_tm(const __grid_constant__ App
 
 // =====================================================================  K-D
 template <int L>
-__global__ void __launch_bounds__(512) k_yinv(const __grid_constant__ ApplyParams p) {
+__global__ void __launch_bounds__(512, 2) k_yinv(const __grid_constant__ ApplyParams p) {
   using P = FftPlan<L>;
   constexpr int T = P::T, V = P::V, R0 = P::radix(0, false), RL = P::radix(P::NST - 1, false);
   extern __shared__ double2 sm[];

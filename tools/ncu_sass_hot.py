@@ -2,16 +2,23 @@
 reasons that dominate each.  usage: python tools/ncu_sass_hot.py report.ncu-rep [N]"""
 import csv
 import io
+import os
 import subprocess
 import sys
 
 rep = sys.argv[1]
 n = int(sys.argv[2]) if len(sys.argv) > 2 else 25
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
-                     capture_output=True, text=True).stdout
+kf = os.environ.get("KREGEX")  # optional kernel filter (regex) for multi-kernel reports
+cmd = ["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"] + (["-k", "regex:" + kf] if kf else [])
+out = subprocess.run(cmd, capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
 hdr = rows[1]
-data = [r for r in rows[2:] if len(r) == len(hdr)]
+data = []
+for r in rows[2:]:  # first kernel section only
+    if r and r[0] == "Kernel Name":
+        break
+    if len(r) == len(hdr):
+        data.append(r)
 ia, isrc, ism = hdr.index("Address"), hdr.index("Source"), hdr.index("Warp Stall Sampling (All Samples)")
 stall_cols = [i for i, h in enumerate(hdr) if h.startswith("stall_")]
 tot = sum(float(r[ism] or 0) for r in data)
