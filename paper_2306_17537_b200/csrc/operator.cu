@@ -486,7 +486,11 @@ __global__ void __launch_bounds__(128, 3) k_zconv16t(const __grid_constant__ App
     for (int m = threadIdx.x; m < L; m += blockDim.x) cp_async16(&twl[m], &p.pw_z[m]);
     const int ixmin = (kx0 + W - 1 <= nx) ? kx0 : Lx - kx0 - (W - 1);
     const double2* g0 = p.ghat + (long long)iy * (nx + 1) + ixmin;
-    // component-major: consecutive threads take consecutive planes of one component
+    // Green rows into L2 for the register-lookahead variants (component-major: consecutive
+    // threads take consecutive planes of one component).  Not with GS: the chunk copies are
+    // issued a forward FFT ahead of use and an early prefetch only costs issue slots and DRAM
+    // bandwidth during the staging (measured: c5 K-C 1.47 -> 1.37 ms without it)
+    if constexpr (!GS)
 #pragma unroll
     for (int comp = 0; comp < 6; ++comp)
       for (int iz = threadIdx.x; iz <= NZ; iz += blockDim.x) {
@@ -757,17 +761,7 @@ __global__ void __launch_bounds__(128, 3) k_zconv_tm(const __grid_constant__ App
         else *d = czero();
       }
     for (int m = threadIdx.x; m < L; m += blockDim.x) cp_async16(&twl[m], &p.pw_z[m]);
-    const int ixmin = (kx0 + W - 1 <= nx) ? kx0 : Lx - kx0 - (W - 1);
-    const double2* g0 = p.ghat + (long long)iy * (nx + 1) + ixmin;
-#pragma unroll
-    for (int comp = 0; comp < 6; ++comp)
-      for (int iz = threadIdx.x; iz <= NZ; iz += blockDim.x) {
-        const double2* row = g0 + comp * gcs + iz * gzs;
-#pragma unroll
-        for (int o = 0; o < W; o += 8) prefetch_l2(row + o);
-        prefetch_l2(row + (W - 1));
-      }
-    cp_async_wait_all();
+    cp_async_wait_all();  // (no L2 prefetch of the Green rows: the chunk copies run a pass ahead)
     tmem_fence_before();
     __syncthreads();
     tmem_fence_after();
@@ -1173,7 +1167,8 @@ static cudaError_t go_zconv16(const ApplyParams& p, cudaStream_t s, int W) {
     // IE_KC_VARIANT: 0 = shared-memory-parked spectra (k_zconv16), 1/2/3 = TMEM-parked with
     // that many multiply steps of Green loads in flight (2: c5 K-C 1.79 -> 1.69 ms), 4/5 = TMEM-
     // parked with the Green planes staged through shared memory (1.53 ms), 6/7 = 4 with the
-    // stage twiddles as products of 6 / 2 loaded powers (1.47 / 1.46 ms, the default)
+    // stage twiddles as products of 6 / 2 loaded powers (1.47 / 1.46 ms; without the early L2
+    // prefetch of the Green rows 1.37 ms: 7 is the default)
     static const int kc = [] {
       const char* e = getenv("IE_KC_VARIANT");
       return e ? atoi(e) : 7;

@@ -1,6 +1,5 @@
-cp build/lib_new.so paper_2306_17537_b200/libie_b200.so
-timeout 900 python -m pytest tests/test_gpu_operator.py -q -x -k "not variants" > gpurun_out/pytest_v.log 2>&1; echo "pytest rc $?"; tail -2 gpurun_out/pytest_v.log
-for rep in 1 2; do for v in old new; do cp build/lib_$v.so paper_2306_17537_b200/libie_b200.so
-timeout 300 python bench.py --steps 20 --warmup 5 --no-dd --no-cpu-baseline --no-layered --no-sweep --no-window --no-cufft > gpurun_out/bench_ab.json 2> gpurun_out/bench_ab.err
-echo "[$v]" $(python -c "import json; d=json.load(open('gpurun_out/bench_ab.json')); print(d['value'], d['ms_per_step'], {k: (v['ms'], v['gbs']) for k, v in d['kernels'].items()})")
-done; done
+python __graft_entry__.py > gpurun_out/build.log 2>&1 || { echo "build failed"; exit 1; }
+for rep in 1 2; do
+for v in "IE_NONE=0" "IE_KNOB=5"; do echo "[$v] $(env $v python tools/time_apply.py --config c4h | tail -1)"; echo "[$v] $(env $v python tools/time_apply.py --config c4h --nrhs 3 | tail -1)"; echo "[$v] $(env $v python tools/time_apply.py --config c3h | tail -1)"; done
+echo "[c5] $(python tools/time_apply.py --config c5 | tail -1)"
+done
