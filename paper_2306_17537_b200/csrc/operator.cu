@@ -1167,11 +1167,12 @@ static cudaError_t go_zconv16(const ApplyParams& p, cudaStream_t s, int W) {
     // IE_KC_VARIANT: 0 = shared-memory-parked spectra (k_zconv16), 1/2/3 = TMEM-parked with
     // that many multiply steps of Green loads in flight (2: c5 K-C 1.79 -> 1.69 ms), 4/5 = TMEM-
     // parked with the Green planes staged through shared memory (1.53 ms), 6/7 = 4 with the
-    // stage twiddles as products of 6 / 2 loaded powers (1.47 / 1.46 ms; without the early L2
-    // prefetch of the Green rows 1.37 ms: 7 is the default)
+    // stage twiddles as products of 6 / 2 loaded powers (1.47 / 1.46 ms; 1.36 without the early
+    // L2 prefetch of the Green rows), 8 = k_zconv_tm<256>, the generalised form of 7 (1.34 ms,
+    // the default)
     static const int kc = [] {
       const char* e = getenv("IE_KC_VARIANT");
-      return e ? atoi(e) : 7;
+      return e ? atoi(e) : 8;
     }();
     if (kc == 1) return go_zconv16t<1>(p, s);
     if (kc == 2) return go_zconv16t<2>(p, s);
