@@ -803,14 +803,20 @@ __global__ void __launch_bounds__(128, 3) k_zconv_tm(const __grid_constant__ App
     dft16<-1, true>(v);
     __syncthreads();  // every input row of component l read before the exchange overwrites it
     if (hook) g_chunk(0, RA);  // blocks 0-1 are free once component 1 is done
+    {  // rows t*16 .. t*16+15 lie on one side of NZ (a multiple of 16): one select per pass
+      double2* wb = xrow(l, t * 16);
 #pragma unroll
-    for (int r = 0; r < 16; ++r) *xrow(l, t * 16 + r) = v[r];
+      for (int r = 0; r < 16; ++r) wb[r * W] = v[r];
+    }
     __syncthreads();
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int j = t + u * T;
+      // rows j + 16 r: below NZ exactly for r < R1/2 (j < 16)
+      const double2* lo = sm + (l * NZ + j) * W + c;
+      const double2* hi = sm + (3 * NZ + j) * W + c - (long long)NZ * W;
 #pragma unroll
-      for (int r = 0; r < R1; ++r) v[u * R1 + r] = *xrow(l, j + 16 * r);
+      for (int r = 0; r < R1; ++r) v[u * R1 + r] = (r < R1 / 2 ? lo : hi)[16 * r * W];
       twiddle(&v[u * R1], R1, j, std::false_type{});
       dftR<R1, -1>(&v[u * R1]);  // v[u R1 + r] = spectrum at kz = j + 16 r
     }
@@ -848,12 +854,13 @@ __global__ void __launch_bounds__(128, 3) k_zconv_tm(const __grid_constant__ App
         tmem_ld4_raw(taddr + 4 * s, raw);
         tmem_ld4_raw(taddr + 64 + 4 * s, raw + 4);
         tmem_wait_ld8(raw);
-        const int kz = t + u * T + 16 * r, iz = kz <= NZ ? kz : L - kz;
-        const double2* gr = R + (iz - CH * k) * W + c;
+        // kz = j + 16 r < NZ for r < R1/2 (j < 16); otherwise iz = L - kz (kz = NZ: its own mirror)
+        const int j = t + u * T;
+        const double2* gr = r < R1 / 2 ? R + (j + 16 * r - CH * k) * W + c : R + (L - j - 16 * r - CH * k) * W + c;
         double2 G[6];
 #pragma unroll
         for (int q6 = 0; q6 < 6; ++q6) G[q6] = gr[q6 * GR * W];
-        const unsigned fz = kz > NZ ? 0x80000000u : 0u;
+        const unsigned fz = (r < R1 / 2 || (r == R1 / 2 && j == 0)) ? 0u : 0x80000000u;
         const double2 gxy = flip_if(G[3], fx ^ fy), gxz = flip_if(G[4], fx ^ fz), gyz = flip_if(G[5], fy ^ fz);
         const double2 j0 = raw_to_z(raw), j1 = raw_to_z(raw + 4), j2 = v[s];
         tmem_st1(taddr + 4 * s, cdot3(G[0], j0, gxy, j1, gxz, j2));

@@ -1,5 +1,3 @@
 python __graft_entry__.py > gpurun_out/build.log 2>&1 || { echo "build failed"; exit 1; }
-for rep in 1 2; do
-for v in "IE_NONE=0" "IE_KNOB=5"; do echo "[$v] $(env $v python tools/time_apply.py --config c4h | tail -1)"; echo "[$v] $(env $v python tools/time_apply.py --config c4h --nrhs 3 | tail -1)"; echo "[$v] $(env $v python tools/time_apply.py --config c3h | tail -1)"; done
-echo "[c5] $(python tools/time_apply.py --config c5 | tail -1)"
-done
+timeout 900 python -m pytest tests/test_gpu_operator.py tests/test_gpu_fullsize.py -q -x -k "not variants" > gpurun_out/pytest_v.log 2>&1; echo "pytest rc $?"; tail -2 gpurun_out/pytest_v.log
+for rep in 1 2 3; do for v in "IE_KC_VARIANT=7" "IE_NONE=0"; do echo "[$v] $(env $v python tools/time_apply.py --config c5 | tail -1)"; done; echo "[c4h] $(python tools/time_apply.py --config c4h | tail -1)"; done
