@@ -110,21 +110,27 @@ __global__ void k_reduce_rows(const double2* __restrict__ part, int nblk, double
   if (threadIdx.x == 0) out[row] = red[0];
 }
 
+// out = base + sum_j coef_j V_j.  Eight basis loads of an element are issued before their FMAs
+// (uniform predicates) so each thread keeps 8 x 16 bytes in flight.
 __global__ void __launch_bounds__(256) k_maxpy(const AxpyJob* __restrict__ jobs, const double2* __restrict__ coefs,
                                                long long len) {
+  constexpr int G = 8;
   const AxpyJob jb = jobs[blockIdx.y];
   __shared__ double2 cf[160];
   for (int j = threadIdx.x; j < jb.nv; j += blockDim.x) cf[j] = coefs[jb.coef + j];
   __syncthreads();
   for (long long i = blockIdx.x * 256LL + threadIdx.x; i < len; i += (long long)gridDim.x * 256) {
     double2 a0 = jb.base ? jb.base[i] : czero(), a1 = czero();
-    int j = 0;
-    for (; j + 1 < jb.nv; j += 2) {
-      const double2 v0 = jb.V[(long long)j * len + i], v1 = jb.V[(long long)(j + 1) * len + i];
-      a0 = cadd(a0, cmul(cf[j], v0));
-      a1 = cadd(a1, cmul(cf[j + 1], v1));
+    for (int j0 = 0; j0 < jb.nv; j0 += G) {
+      double2 v[G];
+#pragma unroll
+      for (int g = 0; g < G; ++g) v[g] = j0 + g < jb.nv ? jb.V[(long long)(j0 + g) * len + i] : czero();
+#pragma unroll
+      for (int g = 0; g < G; g += 2) {
+        if (j0 + g < jb.nv) a0 = cadd(a0, cmul(cf[j0 + g], v[g]));
+        if (j0 + g + 1 < jb.nv) a1 = cadd(a1, cmul(cf[j0 + g + 1], v[g + 1]));
+      }
     }
-    if (j < jb.nv) a0 = cadd(a0, cmul(cf[j], jb.V[(long long)j * len + i]));
     jb.out[i] = cadd(a0, a1);
   }
 }
