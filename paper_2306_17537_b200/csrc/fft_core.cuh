@@ -55,36 +55,52 @@ __device__ __forceinline__ void dft2(double2* v) {
   v[0] = cadd(a, b);
   v[1] = csub(a, b);
 }
-template <int DIR>
+// HALF_IN: the upper half of the inputs is zero (not read); HALF_OUT: only the lower half of the
+// outputs is produced (the others are left unspecified)
+template <int DIR, bool HALF_IN = false, bool HALF_OUT = false>
 __device__ __forceinline__ void dft4(double2& v0, double2& v1, double2& v2, double2& v3) {
-  double2 e0 = cadd(v0, v2), e1 = csub(v0, v2);
-  double2 o0 = cadd(v1, v3), o1 = mul_w4<DIR>(csub(v1, v3));
-  v0 = cadd(e0, o0);
-  v2 = csub(e0, o0);
-  v1 = cadd(e1, o1);
-  v3 = csub(e1, o1);
+  if constexpr (HALF_IN) {  // v2 = v3 = 0
+    const double2 a = v0, b = v1, wb = mul_w4<DIR>(b);
+    v0 = cadd(a, b);
+    v1 = cadd(a, wb);
+    if constexpr (!HALF_OUT) {
+      v2 = csub(a, b);
+      v3 = csub(a, wb);
+    }
+  } else {
+    double2 e0 = cadd(v0, v2), e1 = csub(v0, v2);
+    double2 o0 = cadd(v1, v3), o1 = mul_w4<DIR>(csub(v1, v3));
+    v0 = cadd(e0, o0);
+    v1 = cadd(e1, o1);
+    if constexpr (!HALF_OUT) {
+      v2 = csub(e0, o0);
+      v3 = csub(e1, o1);
+    }
+  }
 }
-template <int DIR>
+template <int DIR, bool HALF_IN = false, bool HALF_OUT = false>
 __device__ __forceinline__ void dft4(double2* v) {
-  dft4<DIR>(v[0], v[1], v[2], v[3]);
+  dft4<DIR, HALF_IN, HALF_OUT>(v[0], v[1], v[2], v[3]);
 }
-template <int DIR>
+template <int DIR, bool HALF_IN = false, bool HALF_OUT = false>
 __device__ __forceinline__ void dft8(double2* v) {
-  double2 e0 = v[0], e1 = v[2], e2 = v[4], e3 = v[6];
-  double2 o0 = v[1], o1 = v[3], o2 = v[5], o3 = v[7];
-  dft4<DIR>(e0, e1, e2, e3);
-  dft4<DIR>(o0, o1, o2, o3);
+  double2 e0 = v[0], e1 = v[2], e2 = HALF_IN ? czero() : v[4], e3 = HALF_IN ? czero() : v[6];
+  double2 o0 = v[1], o1 = v[3], o2 = HALF_IN ? czero() : v[5], o3 = HALF_IN ? czero() : v[7];
+  dft4<DIR, HALF_IN>(e0, e1, e2, e3);  // (v0, v2, v4, v6): upper half v4, v6 zero when HALF_IN
+  dft4<DIR, HALF_IN>(o0, o1, o2, o3);
   o1 = mul_w8<DIR>(o1);
   o2 = mul_w4<DIR>(o2);
   o3 = mul_w83<DIR>(o3);
   v[0] = cadd(e0, o0);
-  v[4] = csub(e0, o0);
   v[1] = cadd(e1, o1);
-  v[5] = csub(e1, o1);
   v[2] = cadd(e2, o2);
-  v[6] = csub(e2, o2);
   v[3] = cadd(e3, o3);
-  v[7] = csub(e3, o3);
+  if constexpr (!HALF_OUT) {
+    v[4] = csub(e0, o0);
+    v[5] = csub(e1, o1);
+    v[6] = csub(e2, o2);
+    v[7] = csub(e3, o3);
+  }
 }
 // multiply by w16 = exp(DIR i pi/8) and w16^3 = exp(3 DIR i pi/8)
 template <int DIR>
@@ -145,12 +161,12 @@ __device__ __forceinline__ void dft16(double2* v) {
   }
 }
 
-template <int R, int DIR>
+template <int R, int DIR, bool HALF_IN = false, bool HALF_OUT = false>
 __device__ __forceinline__ void dftR(double2* v) {
   if constexpr (R == 2) dft2<DIR>(v);
-  else if constexpr (R == 4) dft4<DIR>(v);
-  else if constexpr (R == 8) dft8<DIR>(v);
-  else dft16<DIR>(v);
+  else if constexpr (R == 4) dft4<DIR, HALF_IN, HALF_OUT>(v);
+  else if constexpr (R == 8) dft8<DIR, HALF_IN, HALF_OUT>(v);
+  else dft16<DIR, HALF_IN, HALF_OUT>(v);
 }
 
 // ------------------------------------------------------------------------ plans
@@ -192,7 +208,7 @@ __host__ __device__ constexpr int padded(int n) { return n + (n >> 3); }
 // sm + idx(l)(i): shared-memory slot of element i of line l.  tw: twiddle table of this
 // (L, order).  need_sync_first: a __syncthreads() before the first shared write (when the
 // regions were read just before).  All threads of the CTA must call this (barriers).
-template <int L, bool REV, int DIR, int NL, int S, class IdxF>
+template <int L, bool REV, int DIR, int NL, int S, bool HOUT = false, class IdxF>
 __device__ __forceinline__ void fft_stage(double2 (&v)[NL][FftPlan<L>::V], double2* sm, IdxF idx, int t,
                                           const double2* __restrict__ tw) {
   using P = FftPlan<L>;
@@ -237,7 +253,7 @@ __device__ __forceinline__ void fft_stage(double2 (&v)[NL][FftPlan<L>::V], doubl
 #pragma unroll
       for (int r = 1; r < R; ++r)
         v[l][u * R + r] = (DIR < 0) ? cmul(v[l][u * R + r], w[r]) : cmulc(v[l][u * R + r], w[r]);
-      dftR<R, DIR>(&v[l][u * R]);
+      dftR<R, DIR, false, HOUT && S == NST - 1>(&v[l][u * R]);
     }
   }
   if constexpr (S < NST - 1) {
@@ -253,11 +269,13 @@ __device__ __forceinline__ void fft_stage(double2 (&v)[NL][FftPlan<L>::V], doubl
         for (int r = 0; r < R; ++r) sm[idx(l)(base + r * Ns)] = v[l][u * R + r];
       }
     __syncthreads();
-    fft_stage<L, REV, DIR, NL, S + 1>(v, sm, idx, t, tw);
+    fft_stage<L, REV, DIR, NL, S + 1, HOUT>(v, sm, idx, t, tw);
   }
 }
 
-template <int L, bool REV, int DIR, int NL, class IdxF>
+// HIN: the upper half of every first-stage radix group is zero (zero-padded forward input);
+// HOUT: only the lower half of every last-stage radix group is needed (cropped inverse output)
+template <int L, bool REV, int DIR, int NL, bool HIN = false, bool HOUT = false, class IdxF>
 __device__ __forceinline__ void fft_run(double2 (&v)[NL][FftPlan<L>::V], double2* sm, IdxF idx, int t,
                                         const double2* __restrict__ tw, bool need_sync_first) {
   using P = FftPlan<L>;
@@ -266,7 +284,7 @@ __device__ __forceinline__ void fft_run(double2 (&v)[NL][FftPlan<L>::V], double2
 #pragma unroll
   for (int l = 0; l < NL; ++l)
 #pragma unroll
-    for (int u = 0; u < V / R0; ++u) dftR<R0, DIR>(&v[l][u * R0]);
+    for (int u = 0; u < V / R0; ++u) dftR<R0, DIR, HIN, HOUT && NST == 1>(&v[l][u * R0]);
   if constexpr (NST > 1) {
     if (need_sync_first) __syncthreads();
 #pragma unroll
@@ -278,7 +296,7 @@ __device__ __forceinline__ void fft_run(double2 (&v)[NL][FftPlan<L>::V], double2
         for (int r = 0; r < R0; ++r) sm[idx(l)(j * R0 + r)] = v[l][u * R0 + r];
       }
     __syncthreads();
-    fft_stage<L, REV, DIR, NL, 1>(v, sm, idx, t, tw);
+    fft_stage<L, REV, DIR, NL, 1, HOUT>(v, sm, idx, t, tw);
   }
 }
 

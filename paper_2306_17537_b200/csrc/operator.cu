@@ -84,7 +84,7 @@ __global__ void __launch_bounds__(128, 5) k_xfwd(const __grid_constant__ ApplyPa
     for (int u = 0; u < V / R0; ++u)
 #pragma unroll
       for (int r = 0; r < R0; ++r) v[0][u * R0 + r] = r < R0 / 2 ? J[l][u * (R0 / 2) + r] : czero();
-    fft_run<L, false, -1, 1>(v, sm, idx, t, p.tw_x, l > 0);
+    fft_run<L, false, -1, 1, true>(v, sm, idx, t, p.tw_x, l > 0);
     if (valid) {
       double2* out = p.X1 + ((((long long)blockIdx.y * 3 + l) * p.nz + zz) * p.ny + yy) * L;
 #pragma unroll
@@ -118,7 +118,7 @@ __global__ void __launch_bounds__(512) k_yfwd(const __grid_constant__ ApplyParam
       v[0][u * R0 + r] = (r < R0 / 2 && y >= it.sy0 && y < it.sy1) ? src[(long long)y * Lx] : czero();
     }
   auto idx = [&](int) { return SIdx{0, W, c}; };
-  fft_run<L, false, -1, 1>(v, sm, idx, t, p.tw_y, false);
+  fft_run<L, false, -1, 1, true>(v, sm, idx, t, p.tw_y, false);
   double2* dst = p.X2 + (((long long)item * 3 + q) * p.nz + z) * (long long)L * Xw + (kx - p.k0x);
 #pragma unroll
   for (int u = 0; u < V / RL; ++u)
@@ -924,7 +924,7 @@ __global__ void __launch_bounds__(512, 2) k_yinv(const __grid_constant__ ApplyPa
 #pragma unroll
     for (int r = 0; r < R0; ++r) v[0][u * R0 + r] = src[(long long)(t + u * T + r * (L / R0)) * Xw];
   auto idx = [&](int) { return SIdx{0, W, c}; };
-  fft_run<L, false, +1, 1>(v, sm, idx, t, p.tw_y, false);
+  fft_run<L, false, +1, 1, false, true>(v, sm, idx, t, p.tw_y, false);
   double2* dst = p.X1 + (((long long)item * 3 + q) * p.nz + z) * p.ny * Lx + kx;
 #pragma unroll
   for (int u = 0; u < V / RL; ++u)
@@ -960,7 +960,7 @@ __global__ void __launch_bounds__(128) k_xinv(const __grid_constant__ ApplyParam
   }
   const int region = padded(L);
   auto idx = [&](int) { return SIdx{lr * region, 1, 0}; };
-  fft_run<L, false, +1, 1>(v, sm, idx, t, p.tw_x, false);
+  fft_run<L, false, +1, 1, false, true>(v, sm, idx, t, p.tw_x, false);
   if (!valid) return;
   const long long off = ((long long)zz * ny + yy) * nx;
   const double a = p.alpha * it.xscale, b = p.beta;
