@@ -227,3 +227,40 @@ def test_c2mod_krylov_dd_matches_oracle_gmres(scheme):
     st = ie.ie_solve_dd(ctx, e, scheme, boxes=cfg.boxes, outer_tol=1e-9, restart=30, inner_tol_fixed=1e-2,
                         max_sweeps=100)
     assert rel(e.cpu().numpy()[0], Xref) < FIELD_TOL
+
+
+def _tall_cfg(n, boxes):
+    """Tall grids whose z-pass runs the TMEM kernels (2nz = 256, 128), z-split sub-domains so the
+    Gauss-Seidel coupling applies have z-restricted sources; smooth anisotropic contrast of the
+    c2mod kind (moderate, so the oracle GMRES converges quickly)."""
+    from ie_workloads import Config
+
+    def sig(rng, cfg):
+        nx, ny, nz = cfg.n
+        A = rng.standard_normal((nz, ny, nx, 3, 3)) * 0.05
+        return 0.5 * (A + np.swapaxes(A, -1, -2)) + (cfg.sigma_b * 1.5) * np.eye(3)
+
+    return Config("tall", n, 0.2, 0.3, 4e5, 11, sig,
+                  sources=[(np.array([0.013, 0.021, 0.017]), np.array([0.2, -0.3, 1.0]))],
+                  boxes=boxes, restart=30)
+
+
+@pytest.mark.parametrize("n,boxes", [
+    ((8, 8, 128), [(0, 8, 0, 8, 0, 64), (0, 8, 0, 8, 64, 128)]),
+    ((16, 16, 64), [(0, 16, 0, 16, 0, 32), (0, 16, 0, 16, 32, 48), (0, 16, 0, 16, 48, 64)]),
+])
+@pytest.mark.parametrize("scheme", ["jacobi", "gauss_seidel"])
+def test_tall_grid_dd_matches_oracle_gmres(n, boxes, scheme):
+    """DD on 2nz = 256 / 128 grids (TMEM z-pass with z-restricted coupling sources; unequal
+    z-boxes) at tol 1e-9 vs the oracle's full-domain GMRES at 1e-12."""
+    import paper_2306_17537_b200 as ie
+    cfg = _tall_cfg(n, boxes)
+    ctx, sigma = gpu_ctx(cfg)
+    k0, ds, E0 = oracle_setup(cfg, sigma)
+    Aop = op.Operator(cfg.n, cfg.hvec, k0, cfg.sigma_b, ds)
+    Xref, info = gmres(Aop, E0[0], x0=E0[0], tol=1e-12, restart=30, max_iters=3000)
+    assert info["converged"]
+    e = _field(cfg, 1)
+    st = ie.ie_solve_dd(ctx, e, scheme, boxes=cfg.boxes, outer_tol=1e-9, restart=30, max_sweeps=300)
+    assert st["e_final"] <= 1e-9
+    assert rel(e.cpu().numpy()[0], Xref) < FIELD_TOL

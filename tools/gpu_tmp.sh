@@ -1,7 +1,2 @@
-L=paper_2306_17537_b200/libie_b200.so
-cp build/lib_new.so $L
-timeout 900 python -m pytest tests/test_gpu_operator.py tests/test_gpu_fullsize.py -q -x -k "not variants" > gpurun_out/pytest_v.log 2>&1; echo "pytest rc $?"; tail -2 gpurun_out/pytest_v.log
-for rep in 1 2; do for v in old new; do cp build/lib_$v.so $L
-timeout 300 python bench.py --steps 20 --warmup 5 --no-dd --no-cpu-baseline --no-layered --no-sweep --no-window --no-cufft > gpurun_out/bench_ab.json 2> gpurun_out/bench_ab.err
-echo "[$v]" $(python -c "import json; d=json.load(open('gpurun_out/bench_ab.json')); print(d['value'], d['ms_per_step'], {k: (v['ms'], v['gbs']) for k, v in d['kernels'].items()})")
-done; done
+python __graft_entry__.py > gpurun_out/build.log 2>&1 || { echo "build failed"; exit 1; }
+timeout 900 python -m pytest tests/test_gpu_solve.py -q -x -k "tall" > gpurun_out/pytest_v.log 2>&1; echo "pytest rc $?"; tail -15 gpurun_out/pytest_v.log
