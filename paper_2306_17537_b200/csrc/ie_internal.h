@@ -50,7 +50,6 @@ struct ApplyParams {
   const double2* tw_zr;  // L = 2nz, reversed order
   const double2* pw_z;   // exp(-2 pi i m / 2nz), m < 2nz (radix-16 z-pass)
   const double2* mhat;   // layered background: packed z-z' spectra (layered.cu), else null
-  int knob;  // experiment switch (IE_KNOB, default 0): lets one process A/B a kernel detail
   int n_items;
   ApplyItem items[kMaxItems];
 };

@@ -434,283 +434,7 @@ __global__ void __launch_bounds__(128, 2) k_zconv16(const __grid_constant__ Appl
   }
 }
 
-// K-C, tensor-memory variant for L = 256 (W = 8 pencils, T = 16 threads per pencil).  The
-// forward z-FFT leaves thread t holding kz = t + 16 r (r < 16) of its pencil; the spectra of
-// components 0 and 1 are parked in the thread's own TMEM lane (128 columns), component 2 stays in
-// registers, the 3x3 multiply runs thread-locally, and the inverse starts from those registers --
-// no shared-memory round trip for the parked spectra or the multiply (half the shared-memory
-// wavefronts of k_zconv16).  Shared memory holds the staged inputs (z < nz, 3 components) plus one
-// spare block, reused as the exchange buffers of the radix-16 stages: 68 KB, 3 CTAs per SM.
-// Threads t and 16 - t (mirror partners: kz and L - kz use the same octant Green plane) sit in
-// the same warp so the duplicated Green loads hit L1.
-// GS: the Green planes are staged into shared memory (cp.async, 4 chunks of 33 octant planes,
-// ping-pong between the two halves freed by the forward passes) instead of register lookahead
-// TW: stage twiddles w^(r t) as products w^(4a t) w^(b t) of 6 loaded powers (9 complex
-// multiplies) instead of 15 shared loads
-template <int LA, bool GS = false, int TW = 0>
-__global__ void __launch_bounds__(128, 3) k_zconv16t(const __grid_constant__ ApplyParams p) {
-  constexpr int L = 256, W = 8, T = 16, NZ = 128;
-  constexpr uint32_t kCols = 128;
-  extern __shared__ __align__(16) double2 sm[];
-  double2* twl = sm + 4 * NZ * W;  // exp(-2 pi i m / L), m < L
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(twl + L);
-  const int c = threadIdx.x % W, q = threadIdx.x / W;
-  const int t = (q & 1) ? (q == 1 ? 8 : 16 - (q >> 1)) : (q >> 1);  // warp w: {t, 16 - t} pairs
-  // items fastest in launch order: the CTAs of one pencil tile for all right-hand sides run
-  // together and share its Green rows through L2
-  const int item = p.n_items == 1 ? 0 : blockIdx.x % p.n_items;
-  const int xt = p.n_items == 1 ? blockIdx.x : blockIdx.x / p.n_items;
-  const ApplyItem& it = p.items[item];
-  const int nx = p.nx, ny = p.ny, Lx = 2 * nx, Ly = 2 * ny, Xw = p.x2w;
-  const int kx0 = p.k0x + xt * W, kx = kx0 + c;
-  const int by = blockIdx.y;
-  const int ky = (by == 0) ? 0 : (by == 1 ? ny : ((by & 1) ? Ly - (by >> 1) : (by >> 1)));
-  const long long cs = (long long)NZ * Ly * Xw, zs = (long long)Ly * Xw;
-  double2* tile = p.X2 + (long long)item * 3 * cs + (long long)ky * Xw + (kx0 - p.k0x);
-  const long long gcs = (long long)(NZ + 1) * (ny + 1) * (nx + 1);
-  const long long gzs = (long long)(ny + 1) * (nx + 1);
-  const int ix = kx <= nx ? kx : Lx - kx;
-  const int iy = ky <= ny ? ky : Ly - ky;
-  const double2* g = p.ghat + (long long)iy * (nx + 1) + ix;
-
-  if (threadIdx.x < 32) tmem_alloc(tslot, kCols);
-  {
-    const int z0 = it.sz0, z1 = it.sz1;
-#pragma unroll
-    for (int l = 0; l < 3; ++l)
-      for (int z = t; z < NZ; z += T) {
-        double2* d = &sm[(l * NZ + z) * W + c];
-        if (z >= z0 && z < z1) cp_async16(d, tile + l * cs + z * zs + c);
-        else *d = czero();
-      }
-    for (int m = threadIdx.x; m < L; m += blockDim.x) cp_async16(&twl[m], &p.pw_z[m]);
-    const int ixmin = (kx0 + W - 1 <= nx) ? kx0 : Lx - kx0 - (W - 1);
-    const double2* g0 = p.ghat + (long long)iy * (nx + 1) + ixmin;
-    // Green rows into L2 for the register-lookahead variants (component-major: consecutive
-    // threads take consecutive planes of one component).  Not with GS: the chunk copies are
-    // issued a forward FFT ahead of use and an early prefetch only costs issue slots and DRAM
-    // bandwidth during the staging (measured: c5 K-C 1.47 -> 1.37 ms without it)
-    if constexpr (!GS)
-#pragma unroll
-    for (int comp = 0; comp < 6; ++comp)
-      for (int iz = threadIdx.x; iz <= NZ; iz += blockDim.x) {
-        const double2* row = g0 + comp * gcs + iz * gzs;
-        prefetch_l2(row);
-        prefetch_l2(row + (W - 1));
-      }
-    cp_async_wait_all();
-    tmem_fence_before();
-    __syncthreads();
-    tmem_fence_after();
-  }
-  const uint32_t taddr = *tslot + ((uint32_t)(32 * (threadIdx.x / 32)) << 16);
-
-  // exchange rows of component l's forward pass: rows < NZ in its own staging block, the rest in
-  // the spare block
-  auto xrow = [&](int l, int row) -> double2* {
-    return row < NZ ? sm + (l * NZ + row) * W + c : sm + (3 * NZ + row - NZ) * W + c;
-  };
-  // Green chunk k: octant planes iz in [32k, 32k + 32], layout [6][33][W], own column only
-  constexpr int GR = 33;
-  auto g_chunk = [&](int k, double2* R) {
-    for (int row = t; row < GR; row += T) {
-      const double2* src = g + (32 * k + row) * gzs;
-#pragma unroll
-      for (int comp = 0; comp < 6; ++comp) cp_async16(R + (comp * GR + row) * W + c, src + comp * gcs);
-    }
-    cp_async_commit();
-  };
-  double2* const RA = sm;               // staging blocks 0-1
-  double2* const RB = sm + 2 * NZ * W;  // staging block 2 + spare
-  // v[r] *= w^(r t) (CONJ: conj) for r = 1..15
-  auto twiddle = [&](double2(&v)[16], auto conj_tag) {
-    constexpr bool CONJ = decltype(conj_tag)::value;
-    if constexpr (TW == 2) {  // 2 loads, 4 more multiplies
-      const double2 b1 = twl[t], a1 = twl[4 * t];
-      const double2 b2 = cmul(b1, b1), a2 = cmul(a1, a1);
-      const double2 b3 = cmul(b2, b1), a3 = cmul(a2, a1);
-      const double2 bb[4] = {make_double2(1.0, 0.0), b1, b2, b3};
-      const double2 aa[4] = {make_double2(1.0, 0.0), a1, a2, a3};
-#pragma unroll
-      for (int r = 1; r < 16; ++r) {
-        const int a = r >> 2, b = r & 3;
-        const double2 w = (a == 0) ? bb[b] : (b == 0 ? aa[a] : cmul(aa[a], bb[b]));
-        v[r] = CONJ ? cmulc(v[r], w) : cmul(v[r], w);
-      }
-    } else if constexpr (TW == 1) {
-      const double2 b1 = twl[t], b2 = twl[2 * t], b3 = twl[3 * t];
-      const double2 a1 = twl[4 * t], a2 = twl[8 * t], a3 = twl[12 * t];
-      const double2 bb[4] = {make_double2(1.0, 0.0), b1, b2, b3};
-      const double2 aa[4] = {make_double2(1.0, 0.0), a1, a2, a3};
-#pragma unroll
-      for (int r = 1; r < 16; ++r) {
-        const int a = r >> 2, b = r & 3;
-        const double2 w = (a == 0) ? bb[b] : (b == 0 ? aa[a] : cmul(aa[a], bb[b]));
-        v[r] = CONJ ? cmulc(v[r], w) : cmul(v[r], w);
-      }
-    } else {
-#pragma unroll
-      for (int r = 1; r < 16; ++r) v[r] = CONJ ? cmulc(v[r], twl[r * t]) : cmul(v[r], twl[r * t]);
-    }
-  };
-  auto forward = [&](int l, double2(&v)[16]) {
-#pragma unroll
-    for (int r = 0; r < 8; ++r) v[r] = sm[(l * NZ + t + r * T) * W + c];  // z = t + 16 r < nz
-    dft16<-1, true>(v);
-    __syncthreads();  // every input row of component l read before the exchange overwrites it
-    if (GS && l == 2) g_chunk(0, RA);  // blocks 0-1 are free once component 1 is done
-#pragma unroll
-    for (int r = 0; r < 16; ++r) *xrow(l, t * 16 + r) = v[r];
-    __syncthreads();
-#pragma unroll
-    for (int r = 0; r < 16; ++r) v[r] = *xrow(l, t + 16 * r);
-    twiddle(v, std::false_type{});
-    dft16<-1>(v);  // v[r] = spectrum at kz = t + 16 r
-  };
-  auto tm_put16 = [&](uint32_t col, const double2(&v)[16]) {
-#pragma unroll
-    for (int i = 0; i < 4; ++i) tmem_st4(taddr + col + 16 * i, &v[4 * i]);
-  };
-  auto tm_get16 = [&](uint32_t col, double2(&v)[16]) {
-#pragma unroll
-    for (int i = 0; i < 4; ++i) tmem_ld4(taddr + col + 16 * i, &v[4 * i]);
-  };
-
-  // multiply order: i -> r = i/2 (even i) or 15 - i/2 (odd i), so mirror partners' loads of the
-  // same Green plane issue back to back
-  auto r_of = [](int i) { return (i & 1) ? 15 - (i >> 1) : (i >> 1); };
-  auto load_g = [&](int r, double2(&G)[6]) {
-    const int kz = t + 16 * r, iz = kz <= NZ ? kz : L - kz;
-#pragma unroll
-    for (int k = 0; k < 6; ++k) G[k] = ld2(g + iz * gzs + k * gcs);
-  };
-  const unsigned fx = kx > nx ? 0x80000000u : 0u, fy = ky > ny ? 0x80000000u : 0u;
-
-  double2 v[16];
-#pragma unroll 1
-  for (int l = 0; l < 2; ++l) {  // one copy of the code (instruction-cache footprint)
-    forward(l, v);
-    tm_put16(64 * l, v);
-  }
-  tmem_wait_st();
-  if constexpr (GS) {
-    forward(2, v);
-    __syncthreads();  // block 2 + spare read
-    g_chunk(1, RB);
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      if (k == 0) cp_async_wait<1>();
-      else cp_async_wait<0>();
-      __syncthreads();  // chunk k landed (all threads' copies); chunk k-1 fully consumed
-      if (k == 1) g_chunk(2, RA);
-      if (k == 2) g_chunk(3, RB);
-      const double2* R = (k & 1) ? RB : RA;
-      constexpr int KPW = LA == 2 ? 1 : 2;  // kz per TMEM wait (GS: LA picks 1 or 2)
-#pragma unroll
-      for (int i0 = 4 * k; i0 < 4 * k + 4; i0 += KPW) {
-        uint32_t raw[8 * KPW];
-#pragma unroll
-        for (int h = 0; h < KPW; ++h) {
-          const int r = r_of(i0 + h);
-          tmem_ld4_raw(taddr + 4 * r, raw + 8 * h);
-          tmem_ld4_raw(taddr + 64 + 4 * r, raw + 8 * h + 4);
-        }
-        if constexpr (KPW == 1) tmem_wait_ld8(raw);
-        else tmem_wait_ld16(raw);
-#pragma unroll
-        for (int h = 0; h < KPW; ++h) {
-          const int r = r_of(i0 + h), kz = t + 16 * r, iz = kz <= NZ ? kz : L - kz;
-          const double2* gr = R + (iz - 32 * k) * W + c;
-          double2 G[6];
-#pragma unroll
-          for (int q6 = 0; q6 < 6; ++q6) G[q6] = gr[q6 * GR * W];
-          const unsigned fz = kz > NZ ? 0x80000000u : 0u;
-          const double2 gxy = flip_if(G[3], fx ^ fy), gxz = flip_if(G[4], fx ^ fz), gyz = flip_if(G[5], fy ^ fz);
-          const double2 j0 = raw_to_z(raw + 8 * h), j1 = raw_to_z(raw + 8 * h + 4), j2 = v[r];
-          tmem_st1(taddr + 4 * r, cdot3(G[0], j0, gxy, j1, gxz, j2));
-          tmem_st1(taddr + 64 + 4 * r, cdot3(gxy, j0, G[1], j1, gyz, j2));
-          v[r] = cdot3(gxz, j0, gyz, j1, G[2], j2);
-        }
-      }
-    }
-  } else {
-  double2 Gq[LA][6];  // Green values of the next LA multiply steps, in flight
-#pragma unroll
-  for (int a = 0; a < LA; ++a) load_g(r_of(a), Gq[a]);
-  forward(2, v);
-#pragma unroll
-  for (int s = 0; s < 8; ++s) {  // two kz per step (i = 2s, 2s+1)
-    uint32_t raw[16];
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int r = r_of(2 * s + h);
-      tmem_ld4_raw(taddr + 4 * r, raw + 8 * h);
-      tmem_ld4_raw(taddr + 64 + 4 * r, raw + 8 * h + 4);
-    }
-    tmem_wait_ld16(raw);
-    double2 J[2][2];
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      J[h][0] = raw_to_z(raw + 8 * h);
-      J[h][1] = raw_to_z(raw + 8 * h + 4);
-    }
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int i = 2 * s + h, r = r_of(i);
-      double2 G[6];
-#pragma unroll
-      for (int k = 0; k < 6; ++k) G[k] = Gq[i % LA][k];
-      if (i + LA < 16) load_g(r_of(i + LA), Gq[i % LA]);
-      const int kz = t + 16 * r;
-      const unsigned fz = kz > NZ ? 0x80000000u : 0u;
-      const double2 gxy = flip_if(G[3], fx ^ fy), gxz = flip_if(G[4], fx ^ fz), gyz = flip_if(G[5], fy ^ fz);
-      const double2 j0 = J[h][0], j1 = J[h][1], j2 = v[r];
-      J[h][0] = cdot3(G[0], j0, gxy, j1, gxz, j2);
-      J[h][1] = cdot3(gxy, j0, G[1], j1, gyz, j2);
-      v[r] = cdot3(gxz, j0, gyz, j1, G[2], j2);
-    }
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int r = r_of(2 * s + h);
-      tmem_st1(taddr + 4 * r, J[h][0]);
-      tmem_st1(taddr + 64 + 4 * r, J[h][1]);
-    }
-  }
-  }
-  tmem_wait_st();
-
-  // inverse z-FFT from registers: radix 16 over r, exchange, twiddle + radix 16, crop, store
-  auto inverse = [&](int l, double2(&v)[16], double2* B) {
-    dft16<+1>(v);
-#pragma unroll
-    for (int r = 0; r < 16; ++r) B[(t * 16 + r) * W + c] = v[r];
-    __syncthreads();
-#pragma unroll
-    for (int r = 0; r < 16; ++r) v[r] = B[(t + r * T) * W + c];
-    twiddle(v, std::true_type{});  // exp(+2 pi i r t / L)
-    dft16<+1, false, true>(v);
-    double2* dst = tile + l * cs + c;
-#pragma unroll
-    for (int r = 0; r < 8; ++r) dst[(long long)(t + r * T) * zs] = v[r];  // z = t + 16 r < nz
-  };
-  // buffers: component 2 -> staging blocks 0-1, component 0 -> block 2 + spare, component 1 ->
-  // blocks 0-1 again (one barrier per component separates each reuse)
-  inverse(2, v, sm);
-#pragma unroll 1
-  for (int l = 0; l < 2; ++l) {
-    tm_get16(64 * l, v);
-    inverse(l, v, l == 0 ? sm + 2 * NZ * W : sm);
-  }
-  tmem_fence_before();
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    tmem_fence_after();
-    tmem_dealloc(*tslot, kCols);
-  }
-}
-
-// K-C, TMEM-parked z-pass for L = 2nz in {128, 256} (the design of k_zconv16t<1, true, 2>,
-// generalised): T = L/16 threads per pencil, W = 2048/L pencils per CTA (128 threads, one TMEM
+// K-C, TMEM-parked z-pass for L = 2nz in {128, 256}: T = L/16 threads per pencil, W = 2048/L pencils per CTA (128 threads, one TMEM
 // lane each).  Forward: radix 16 (first stage, half the inputs zero) then U = 16/R1 radix-R1
 // stages per thread (R1 = L/16), after which thread t holds kz = j + 16 r for j = t + u T
 // (u < U, r < R1): 16 values per component.  Components 0, 1 are parked in the thread's TMEM lane,
@@ -1151,14 +875,6 @@ static cudaError_t go_zconv16_w(const ApplyParams& p, cudaStream_t s) {
   k_zconv16<L, W><<<dim3(p.n_items * (p.x2w / W), 2 * p.ny), W * (L / 16), smem, s>>>(p);
   return cudaGetLastError();
 }
-template <int LA, bool GS = false, int TW = 0>
-static cudaError_t go_zconv16t(const ApplyParams& p, cudaStream_t s) {
-  const size_t smem = (size_t)(4 * 128 * 8 + 256 + 1) * sizeof(double2);
-  cudaError_t e = prep((const void*)k_zconv16t<LA, GS, TW>, smem);
-  if (e) return e;
-  k_zconv16t<LA, GS, TW><<<dim3(p.n_items * (p.x2w / 8), 2 * p.ny), 128, smem, s>>>(p);
-  return cudaGetLastError();
-}
 template <int L>
 static cudaError_t go_zconv_tm(const ApplyParams& p, cudaStream_t s) {
   constexpr int W = 2048 / L;
@@ -1171,24 +887,14 @@ static cudaError_t go_zconv_tm(const ApplyParams& p, cudaStream_t s) {
 static cudaError_t go_zconv16(const ApplyParams& p, cudaStream_t s, int W) {
   const int L = 2 * p.nz;
   if (L == 256) {
-    // IE_KC_VARIANT: 0 = shared-memory-parked spectra (k_zconv16), 1/2/3 = TMEM-parked with
-    // that many multiply steps of Green loads in flight (2: c5 K-C 1.79 -> 1.69 ms), 4/5 = TMEM-
-    // parked with the Green planes staged through shared memory (1.53 ms), 6/7 = 4 with the
-    // stage twiddles as products of 6 / 2 loaded powers (1.47 / 1.46 ms; 1.36 without the early
-    // L2 prefetch of the Green rows), 8 = k_zconv_tm<256>, the generalised form of 7 (1.34 ms,
-    // the default)
+    // IE_KC_VARIANT=0 selects the shared-memory-parked z-pass k_zconv16<256, 8> (1.79 ms on c5)
+    // instead of the TMEM-parked k_zconv_tm<256> (1.34 ms); DESIGN.md section 6 has the steps
+    // between them
     static const int kc = [] {
       const char* e = getenv("IE_KC_VARIANT");
       return e ? atoi(e) : 8;
     }();
-    if (kc == 1) return go_zconv16t<1>(p, s);
-    if (kc == 2) return go_zconv16t<2>(p, s);
-    if (kc == 3) return go_zconv16t<3>(p, s);
-    if (kc == 4) return go_zconv16t<1, true>(p, s);
-    if (kc == 5) return go_zconv16t<2, true>(p, s);
-    if (kc == 6) return go_zconv16t<1, true, 1>(p, s);
-    if (kc == 7) return go_zconv16t<1, true, 2>(p, s);
-    if (kc == 8) return go_zconv_tm<256>(p, s);
+    if (kc != 0) return go_zconv_tm<256>(p, s);
     return go_zconv16_w<256, 8>(p, s);
   }
   // 8-pencil tiles (128-byte rows): more, smaller CTAs per SM measured faster than 128-thread
@@ -1416,11 +1122,6 @@ ie_status launch_apply(ie_ctx* c, ApplyParams& p) {
   p.pw_z = c->tw.powers(2 * p.nz);
   p.x2w = 2 * p.nx;
   p.k0x = 0;
-  static const int knob = [] {
-    const char* e = getenv("IE_KNOB");
-    return e ? atoi(e) : 0;
-  }();
-  p.knob = knob;
   const int S = c->slabs ? slab_width(p) : 0;  // off unless IE_SLABS=1 (measured slower)
   cudaError_t e = S ? run_apply_slabs(c, p, c->stream, S) : run_apply(c, p, c->stream);
   if (e != cudaSuccess) return cuda_fail(c, e, "operator kernels");
