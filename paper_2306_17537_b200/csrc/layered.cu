@@ -325,16 +325,32 @@ __global__ void __launch_bounds__(288, 2) k_zlayer_tma(const __grid_constant__ A
     }
     return;
   }
-  // ---- consumers: stage X (signs applied), then the DMMA loop
-  for (int e = threadIdx.x; e < R * NS; e += NCW * 32) {
-    const int slot = e % NS, row = e / NS, q = row / nz, kp = row % nz;
-    const int item = slot % NI, cc = slot / NI, cx = cc & 1, cy = cc >> 1;
-    double2 v = czero();
-    if (item < p.n_items && cx < nkx && cy < nky && kp >= z0 && kp < z1) {
-      v = p.X2[(long long)item * 3 * cs + q * cs + kp * zs + (long long)kys[cy] * Lx + kxs[cx]];
-      if ((q == 0 && cx == 1) || (q == 1 && cy == 1)) v = make_double2(-v.x, -v.y);
+  // ---- consumers: stage X (signs applied), then the DMMA loop.  The gathers (one 16-byte
+  // element per (row, slot), scattered over the four mirror columns) go out in batches of BT
+  // loads per thread before any is used, so their latencies overlap
+  constexpr int BT = 6;
+  for (int e0 = threadIdx.x; e0 < R * NS; e0 += BT * NCW * 32) {
+    double2 v[BT];
+    bool neg[BT];
+#pragma unroll
+    for (int b = 0; b < BT; ++b) {
+      const int e = e0 + b * NCW * 32;
+      v[b] = czero();
+      neg[b] = false;
+      if (e < R * NS) {
+        const int slot = e % NS, row = e / NS, q = row / nz, kp = row % nz;
+        const int item = slot % NI, cc = slot / NI, cx = cc & 1, cy = cc >> 1;
+        if (item < p.n_items && cx < nkx && cy < nky && kp >= z0 && kp < z1) {
+          v[b] = __ldg(&p.X2[(long long)item * 3 * cs + q * cs + kp * zs + (long long)kys[cy] * Lx + kxs[cx]]);
+          neg[b] = (q == 0 && cx == 1) || (q == 1 && cy == 1);
+        }
+      }
     }
-    xs[e] = v;
+#pragma unroll
+    for (int b = 0; b < BT; ++b) {
+      const int e = e0 + b * NCW * 32;
+      if (e < R * NS) xs[e] = neg[b] ? make_double2(-v[b].x, -v[b].y) : v[b];
+    }
   }
   asm volatile("bar.sync 1, %0;" ::"n"(NCW * 32));  // consumers only
   const int ar = lane >> 2, ac = lane & 3;
