@@ -42,3 +42,15 @@ def test_replicas_take_the_slowest_rank_and_sum_the_work():
     assert [o[1] for o in out] == [5.0, 5.0]
     # 2 replicas x 10 steps x 1 GB in 5 ms -> 4000 GB/s
     assert all(abs(o[2] - 4000.0) < 1e-9 for o in out)
+
+
+def test_bench_accounting_is_consistent():
+    """The per-kernel algorithmic bytes add up to B_model (SURVEY 8(a): 1344 N + 96 (nx+1)(ny+1)(nz+1));
+    the K-C flop count is 6 FFTs of 5 L log2 L plus 72 flops per kz, per pencil of the padded xy grid."""
+    import math
+    import bench
+    for n in [(256, 256, 128), (128, 128, 64), (8, 8, 8)]:
+        assert sum(bench.kernel_bytes(*n).values()) == bench.b_model(*n)
+        L = 2 * n[2]
+        assert bench.kc_flops(*n) == 4 * n[0] * n[1] * (30 * L * math.log2(L) + 72 * L)
+    assert abs(bench.FP64_NOMINAL_TFLOPS - 37.22496) < 1e-9
