@@ -492,7 +492,8 @@ def run_ours(args, cfg, sigma, rank, ws, local):
         # and the Krylov-accelerated DD (FGMRES preconditioned by one sweep, *_fgmres)
         for scheme, adaptive, pc in (("full", True, 0), ("gauss_seidel", False, 0), ("gauss_seidel", True, 0),
                                      ("jacobi", True, 0), ("full", True, 1), ("gauss_seidel", True, 1),
-                                     ("fgmres_jacobi", True, 0), ("fgmres_gauss_seidel", True, 0)):
+                                     ("fgmres_jacobi", True, 0), ("fgmres_gauss_seidel", True, 0),
+                                     ("fgmres_jacobi", True, 1), ("fgmres_gauss_seidel", True, 1)):
             times = []
             st = None
             for rep in range(1 + args.dd_reps):
