@@ -2,9 +2,11 @@
 // P:60-74) as five sm_100a kernels over a 2x zero-padded grid:
 //   K-A k_xfwd : J = dsigma * x fused into the load, zero-pad x, length-2nx forward FFT
 //   K-B k_yfwd : zero-pad y, length-2ny forward FFT (tiles of W consecutive kx)
-//   K-C k_zconv: per (kx,ky) column: forward z FFT (upper half zero) -> 3x3 spectral
-//                multiply with the packed Green spectrum (in registers) -> inverse z FFT
-//                -> crop; written in place
+//   K-C per (kx,ky) column: forward z FFT (upper half zero) -> 3x3 spectral multiply with
+//       the packed Green spectrum -> inverse z FFT -> crop; written in place.
+//       k_zconv_tm (2nz = 128, 256; the default): spectra parked in tensor memory, Green
+//       planes staged through shared memory; k_zconv16 (radix 16, 2nz = 64 and the
+//       IE_KC_VARIANT=0 / IE_KC128_VARIANT=0 baseline); k_zconv (generic lengths)
 //   K-D k_yinv : inverse y FFT, keep the first ny rows
 //   K-E k_xinv : inverse x FFT, keep the first nx, y = alpha*x + beta*conv (+ y)
 // The 1/(8 nx ny nz) normalisation is folded into the packed spectrum (green.cu).
@@ -25,12 +27,6 @@
 namespace ie {
 
 __device__ __forceinline__ double2 ld2(const double2* p) { return __ldg(p); }
-// read-only load that does not allocate in L1 (streamed data must not evict L1-resident tables)
-__device__ __forceinline__ double2 ld2_stream(const double2* p) {
-  double2 v;
-  asm("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
-  return v;
-}
 
 // =====================================================================  K-A
 template <int L>
