@@ -379,6 +379,10 @@ __global__ void __launch_bounds__(288, 2) k_zlayer_tma(const __grid_constant__ A
         }
       }
     }
+    // the ring slot is refilled by the TMA (async proxy) after this release: order this warp's
+    // generic-proxy reads of it first (without the fence a refill could overtake them; seen as
+    // corrupted rows on nz = 64, 1 RHS)
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[st]);
   }

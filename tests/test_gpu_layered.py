@@ -63,7 +63,9 @@ def test_layer_spectrum_matches_oracle(n):
     assert rel(got, ref) < TOL
 
 
-@pytest.mark.parametrize("n", [(8, 4, 4), (4, 8, 2), (16, 8, 8), (8, 8, 32), (1, 2, 4)])
+# nz = 64 / 128 run the TMA-ring DMMA kernel (k_zlayer_tma, 3nz/8 = 24 / 48 row tiles, the c3/c4
+# path); nz = 32 the DMMA-from-global kernel; the small shapes the DFMA kernel
+@pytest.mark.parametrize("n", [(8, 4, 4), (4, 8, 2), (16, 8, 8), (8, 8, 32), (1, 2, 4), (4, 4, 64), (2, 2, 128)])
 @pytest.mark.parametrize("nrhs", [1, 3, 5])
 def test_layered_apply_matches_oracle_random_table(n, nrhs):
     cfg = _cfg(n)
@@ -78,7 +80,7 @@ def test_layered_apply_matches_oracle_random_table(n, nrhs):
         assert rel(y[r], A(x[r])) < TOL
 
 
-@pytest.mark.parametrize("n", [(16, 8, 8), (8, 8, 16)])
+@pytest.mark.parametrize("n", [(16, 8, 8), (8, 8, 16), (16, 16, 64)])
 def test_degenerate_tables_reproduce_the_homogeneous_operator(n):
     """format 2 (library-built degenerate table) and format 1 (the oracle's degenerate table)
     through K-C' equal the homogeneous K-A..K-E operator (Eq. 10)."""
