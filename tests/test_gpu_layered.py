@@ -96,9 +96,12 @@ def test_degenerate_tables_reproduce_the_homogeneous_operator(n):
     assert rel(y_2, y_h) < TOL and rel(y_1, y_h) < TOL
 
 
-@pytest.mark.parametrize("box", [(0, 8, 0, 4, 0, 4), (8, 16, 4, 8, 4, 8), (0, 16, 0, 8, 2, 4)])
-def test_layered_box_operator_is_the_diagonal_block(box):
-    n = (16, 8, 8)
+@pytest.mark.parametrize("n,box", [((16, 8, 8), (0, 8, 0, 4, 0, 4)), ((16, 8, 8), (8, 16, 4, 8, 4, 8)),
+                                   ((16, 8, 8), (0, 16, 0, 8, 2, 4)),
+                                   # 64-deep boxes of a 128-deep grid: the TMA-ring kernel with a
+                                   # layer offset (the z-z' spectra depend on the box's first layer)
+                                   ((4, 4, 128), (0, 4, 0, 4, 64, 128)), ((4, 4, 128), (0, 2, 2, 4, 0, 64))])
+def test_layered_box_operator_is_the_diagonal_block(n, box):
     cfg = _cfg(n)
     rng = np.random.default_rng(4)
     Tq = lay.random_table(n, rng, scale=0.02)
