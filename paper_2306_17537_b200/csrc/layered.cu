@@ -363,22 +363,27 @@ __global__ void __launch_bounds__(288, 2) k_zlayer_tma(const __grid_constant__ A
     const int st = ch % NST;
     mbar_wait(&full[st], (ch / NST) & 1);
     const double2* A = ring + st * KC * R;
+    // all operands of the chunk's KC/4 k-steps loaded before the first DMMA (their shared-memory
+    // latencies overlap)
+    double b[KC / 4][NT];
+    double2 a[KC / 4][RT];
 #pragma unroll
-    for (int kk = 0; kk < KC; kk += 4) {
-      const int k0 = ch * KC + kk;
-      double b[NT];
+    for (int h = 0; h < KC / 4; ++h) {
+      const int k0 = ch * KC + 4 * h;
 #pragma unroll
-      for (int t = 0; t < NT; ++t) b[t] = xd[(k0 + ac) * (2 * NS) + t * 8 + ar];
+      for (int t = 0; t < NT; ++t) b[h][t] = xd[(k0 + ac) * (2 * NS) + t * 8 + ar];
 #pragma unroll
-      for (int r = 0; r < RT; ++r) {
-        const double2 a = A[(kk + ac) * R + (warp + r * NCW) * 8 + ar];
+      for (int r = 0; r < RT; ++r) a[h][r] = A[(4 * h + ac) * R + (warp + r * NCW) * 8 + ar];
+    }
+#pragma unroll
+    for (int h = 0; h < KC / 4; ++h)
+#pragma unroll
+      for (int r = 0; r < RT; ++r)
 #pragma unroll
         for (int t = 0; t < NT; ++t) {
-          dmma(c1[r][t][0], c1[r][t][1], a.x, b[t]);
-          dmma(c2[r][t][0], c2[r][t][1], a.y, b[t]);
+          dmma(c1[r][t][0], c1[r][t][1], a[h][r].x, b[h][t]);
+          dmma(c2[r][t][0], c2[r][t][1], a[h][r].y, b[h][t]);
         }
-      }
-    }
     // the ring slot is refilled by the TMA (async proxy) after this release: order this warp's
     // generic-proxy reads of it first (without the fence a refill could overtake them; seen as
     // corrupted rows on nz = 64, 1 RHS)
