@@ -290,7 +290,9 @@ __global__ void __launch_bounds__(256) k_zlayer_mma(const __grid_constant__ Appl
 template <int NI, int RT>
 __global__ void __launch_bounds__(288, 2) k_zlayer_tma(const __grid_constant__ ApplyParams p) {
   constexpr int NS = 4 * NI, NT = NI;      // slots; real columns 2 NS = 8 NI: NI n-tiles
-  constexpr int KC = 8, NST = 2, NCW = 8;  // k-rows per chunk, ring stages, consumer warps
+  // k-rows per chunk, ring stages (3 for one RHS, where the consumers outpace a 2-deep ring;
+  // 2 otherwise: c3h 1 RHS 0.517 -> 0.506 ms, 3 RHS 0.735 vs 0.760 ms), consumer warps
+  constexpr int KC = 8, NST = NI == 1 ? 3 : 2, NCW = 8;
   extern __shared__ __align__(128) double2 smem[];
   const int nx = p.nx, ny = p.ny, nz = p.nz, Lx = 2 * nx, Ly = 2 * ny, R = 3 * nz;
   double2* xs = smem;                     // [R][NS] complex = [R][2NS] real
@@ -410,7 +412,8 @@ __global__ void __launch_bounds__(288, 2) k_zlayer_tma(const __grid_constant__ A
 template <int NI, int RT>
 static cudaError_t go_zlayer_tma(const ApplyParams& p, cudaStream_t s) {
   const int R = 3 * p.nz;
-  const size_t smem = (size_t)(R * 4 * NI + 2 * 8 * R) * sizeof(double2) + 4 * sizeof(uint64_t);
+  constexpr int NST = NI == 1 ? 3 : 2;  // as in the kernel
+  const size_t smem = (size_t)(R * 4 * NI + NST * 8 * R) * sizeof(double2) + 2 * NST * sizeof(uint64_t);
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute((const void*)k_zlayer_tma<NI, RT>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
