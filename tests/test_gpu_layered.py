@@ -168,3 +168,22 @@ def test_layered_solves_match_dense_lu(scheme):
         ref = np.array([lay.receiver_coupling(X[s], ds, e0rx[d], h0[s, d], dv, physics.omega_of(cfg.freq))
                         for d in range(len(dips))])
         assert rel(H[s], ref) < 1e-6
+
+
+@pytest.mark.parametrize("scheme", ["full", "jacobi", "gauss_seidel"])
+def test_deep_layered_solves_match_dense_lu(scheme):
+    """A 128-deep two-layer grid split into two 64-deep boxes: every sub-domain apply runs the
+    TMA-ring contraction with a layer offset (the upper box starts at layer 64)."""
+    import torch
+    import paper_2306_17537_b200 as ie
+    n = (2, 2, 128)
+    cfg, layers, z_if, Tq, sig, ds, E0, k0, pts = _layered_problem(n)
+    boxes = [(0, 2, 0, 2, 0, 64), (0, 2, 0, 2, 64, 128)]
+    ctx = _ctx(cfg, sig, table=Tq, layers=layers, z_iface=z_if, nrhs=2, boxes=boxes, restart=30)
+    ie.ie_set_incident(ctx, torch.from_numpy(E0).cuda())
+    A = lay.dense_matrix_layered(Tq, ds)
+    X = np.stack([np.linalg.solve(A, e.ravel()).reshape(e.shape) for e in E0])
+    e = torch.empty(E0.shape, dtype=torch.complex128, device="cuda")
+    st = ie.ie_solve_dd(ctx, e, scheme, boxes=boxes, outer_tol=1e-10, restart=30, max_sweeps=300)
+    assert st["e_final"] <= 1e-10
+    assert rel(e.cpu().numpy(), X) < 1e-6
