@@ -4,8 +4,9 @@ H(r) = H^(0)(r) + sum_c G^H(r, r_c) dsigma_c E_c dv   (Eq. 4; "straightfor
 addition").  With Eq. 6, G^H J = (i omega mu0)^-1 curl(G^E J) = grad g x J, so the
 scattered part is sum_c g(R)(i k0 - 1/R) (Rhat x J_c) dv with R = r - r_c; a term with
 R = 0 is 0 (odd kernel over the equivolume ball; reading R13).
-Voltage of a unit receiver coil along m_r: V = i omega mu0 m_r . H (reading R14, parity
-unpinned beyond H).
+Voltage of a unit receiver coil along m_r: V = i omega mu0 m_r . H (reading R14), pinned by
+Faraday's law (Eq. 1) in tests/test_oracle_pins.py: it equals the loop integral of E around a
+small coil of area |m_r|, sign included, for the incident and the scattered fields.
 """
 
 import numpy as np
@@ -35,5 +36,6 @@ def receiver_H(n, h, origin, k0, sigma_b, dsigma, E, rx, src_pos, moment):
 
 
 def voltage(H, m_r, freq_hz):
-    """V = i omega mu0 m_r . H (EMF of a unit-moment coil; reading R14, parity unpinned)."""
+    """V = i omega mu0 m_r . H (EMF of a coil of area |m_r| along m_r; reading R14; pinned by the
+    Faraday loop integral, tests/test_oracle_pins.py)."""
     return 1j * physics.omega_of(freq_hz) * physics.MU0 * np.sum(np.asarray(m_r) * H, axis=-1)

@@ -716,9 +716,9 @@ ie_status ie_solve_dd(ie_ctx* c, const ie_dd_opts* o, void* e_dev, int32_t init_
           g[k + 1] = -std::conj(sn[k]) * g[k];
           g[k] = cs[k] * g[k];
           ++it;
-          ++outer;
+          outer = std::max(outer, it);  // stats->sweeps = the largest per-source count
           const double est = std::abs(g[k + 1]) / bnorm;
-          if (stats->e_hist && outer <= o->max_sweeps) stats->e_hist[(size_t)outer * ns + r] = est;
+          if (stats->e_hist && it <= o->max_sweeps) stats->e_hist[(size_t)it * ns + r] = est;
           if (hk1 > 0) launch_axpby(c, Vj(k + 1), 1.0 / hk1, Vj(k + 1), 0.0, nullptr, len);
           if (est <= o->outer_tol || !(hk1 > 1e-14 * std::abs(Hk[k]))) {
             ++k;

@@ -316,8 +316,9 @@ void launch_scatter(ie_ctx* c, double2* full, const double2* box, const ie_box& 
 }
 
 // z = a x + b y (y may be null)
-__global__ void k_axpby(double2* __restrict__ z, double2 a, const double2* __restrict__ x, double2 b,
-                        const double2* __restrict__ y, long long n) {
+// called in place (z == x or z == y): no __restrict__ on the three vectors (each element is read
+// and written by the same thread)
+__global__ void k_axpby(double2* z, double2 a, const double2* x, double2 b, const double2* y, long long n) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
     double2 v = cmul(a, x[i]);
     if (y) v = cadd(v, cmul(b, y[i]));
@@ -393,7 +394,7 @@ ie_status ensure_precond(ie_ctx* c) {
 }
 
 // y = M x per cell; M sym6 over the grid (strides cs, zs, ys), x and y compact over the box
-__global__ void k_cellmat(double2* __restrict__ y, const double2* __restrict__ x, const double* __restrict__ M, int bx,
+__global__ void k_cellmat(double2* y, const double2* x, const double* __restrict__ M, int bx,
                           int by, int bz, long long cs, long long zs, long long ys) {
   const long long Nb = (long long)bx * by * bz;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < Nb; i += (long long)gridDim.x * blockDim.x) {

@@ -475,7 +475,10 @@ static int zlayer_mode() {
 // repeated launches
 cudaError_t launch_zlayer(const ApplyParams& p, cudaStream_t s) {
   ApplyParams q = p;
-  const int group = (p.nz % 64 == 0 && zlayer_mode() == 0) ? 3 : 4;  // the DMMA kernel is best at <= 3
+  // the TMA-ring kernel is instantiated for 3nz/8 = 24 or 48 row tiles (nz = 64 or 128) only;
+  // every other depth takes the direct-load DMMA or the DFMA kernel
+  const bool tma = (p.nz == 64 || p.nz == 128) && zlayer_mode() == 0;
+  const int group = tma ? 3 : 4;  // the DMMA kernel is best at <= 3
   for (int i0 = 0; i0 < p.n_items; i0 += group) {
     const int ni = std::min(group, p.n_items - i0);
     q.n_items = ni;
@@ -484,7 +487,7 @@ cudaError_t launch_zlayer(const ApplyParams& p, cudaStream_t s) {
     q.X2 = p.X2 + (long long)i0 * per_item;
     cudaError_t e;
     const int mode = zlayer_mode();
-    if (p.nz % 64 == 0 && mode == 0)  // DMMA fed by the TMA ring (3nz/8 row tiles over 8 warps)
+    if (tma)  // DMMA fed by the TMA ring (3nz/8 row tiles over 8 warps)
       e = ni == 1 ? go_zlayer_tma_r<1>(q, s) : ni == 2 ? go_zlayer_tma_r<2>(q, s)
                   : ni == 3 ? go_zlayer_tma_r<3>(q, s) : go_zlayer_tma_r<4>(q, s);
     else if (ni >= 2 && p.nz % 8 == 0 && mode <= 1)  // DMMA, operands straight from global
