@@ -9,6 +9,10 @@ DESIGN.md §Inputs; variants:
             sigma_v down to 1e-3 S/m against sigma_b = 0.1, are the cause, not the cap)
   c2mod     the c2 geometry with moderate contrast: sigma_h = sigma_b 10^U[-0.3,0.7],
             sigma_v/sigma_h ~ U[0.3,1] (oracle GMRES(30) reaches 1e-11 in 56 iterations)
+  c3, c4    the layered configs as BASELINE.json specifies them: three layers 1 / 0.01 / 1 S/m
+            with interfaces at -4 / +4 m; tables and incident fields from layered_green (input data)
+  c3capped  c3 with d_i <= min(5, 10 sigma_b(z))
+  c3lmini, c4lmini  the c3 / c4 recipes on 8^3 with the interfaces scaled to -0.5 / +0.5 m
   c3h, c4h  the c3 / c4 grids, contrast recipes and tools on a HOMOGENEOUS background
             (c3h: sigma_b = 1 S/m; c4h: sigma_b = 0.01 S/m, the middle layer that holds the
             slab and the trajectory -- in a 1 S/m host the sigma_v = 0.005 slab is a 200x
@@ -41,6 +45,25 @@ class Config:
     outer_tol: float = 1e-8
     parity_tol: float = 1e-9
     note: str = ""
+    layers: Tuple = None             # layered background: sigma per layer, bottom -> top (S/m)
+    z_iface: Tuple = None            # ascending interface depths (m); sigma_b is None then
+    rx_moments: Tuple = None         # receiver dipole axes (rows); default x, y, z
+
+    @property
+    def layered(self):
+        return self.layers is not None
+
+    def background(self):
+        """(sigma per layer, interfaces) -- a one-layer tuple for a homogeneous background."""
+        if self.layered:
+            return tuple(self.layers), tuple(self.z_iface)
+        return (self.sigma_b,), ()
+
+    def sigma_b_at(self, z):
+        """Background conductivity at depth(s) z (layer l holds z_iface[l-1] <= z < z_iface[l])."""
+        lay, zi = self.background()
+        return np.asarray(lay, np.float64)[np.searchsorted(np.asarray(zi, np.float64), np.asarray(z, np.float64),
+                                                          side="right")]
 
     @property
     def hvec(self):
@@ -164,6 +187,48 @@ def _c5_sigma(rng, cfg, corr_len=2.0, spread=0.3, block=10):
     return 0.5 * (s + np.swapaxes(s, -1, -2))  # exactly symmetric
 
 
+def _c3_sigma_capped(rng, cfg, block=16):
+    """c3capped: as c3 but d_i = 10^(-2 + u (hi(z) + 2)), u ~ U[0,1] per cell
+    (the same draws as c3), hi(z) = log10 min(5, 10 sigma_b(z)): contrast <= 9 sigma_b."""
+    nx, ny, nz = cfg.n
+    nbx, nby, nbz = -(-nx // block), -(-ny // block), -(-nz // block)
+    Rs = np.stack([haar_rotation(rng) for _ in range(nbx * nby * nbz)]).reshape(nbz, nby, nbx, 3, 3)
+    u = rng.uniform(0.0, 1.0, size=(nz, ny, nx, 3))
+    hi = np.log10(np.minimum(5.0, 10.0 * cfg.sigma_b_at(cfg.cell_centers(2))))
+    d = 10.0 ** (-2.0 + u * (hi[:, None, None, None] + 2.0))
+    iz, iy, ix = np.meshgrid(np.arange(nz) // block, np.arange(ny) // block, np.arange(nx) // block, indexing="ij")
+    R = Rs[iz, iy, ix]
+    s = np.einsum("zyxij,zyxj,zyxkj->zyxik", R, d, R)
+    return 0.5 * (s + np.swapaxes(s, -1, -2))
+
+
+def _c4_sigma_layered(rng, cfg, slab_half=1.0, inset=2.0, n_ell=20, axes=(0.5, 2.0)):
+    """c4 (layered, BASELINE.json configs[3]): background sigma_b(z) of the three layers, then a
+    slab of half-thickness 1 m through the origin with normal (sin30, 0, cos30), TI sigma_h = 0.02,
+    sigma_v = 0.005 about the normal (App. C, theta = 30 deg, phi = 0); then 20 ellipsoids:
+    centre U over the grid inset 2 m, semi-axes U[0.5, 2] m, Haar rotation, eigenvalues
+    sigma_b(centre) 10^U[-1, 1]; later objects overwrite earlier ones."""
+    nx, ny, nz = cfg.n
+    z, y, x = (cfg.cell_centers(2), cfg.cell_centers(1), cfg.cell_centers(0))
+    s = np.zeros((nz, ny, nx, 3, 3))
+    s[...] = cfg.sigma_b_at(z)[:, None, None, None, None] * np.eye(3)
+    Z, Y, X = np.meshgrid(z, y, x, indexing="ij")
+    nrm = np.array([np.sin(np.radians(30)), 0.0, np.cos(np.radians(30))])
+    slab = np.abs(X * nrm[0] + Y * nrm[1] + Z * nrm[2]) <= slab_half
+    s[slab] = vti_tensor(0.02, 0.005, np.radians(30.0), 0.0)
+    lo = np.array([x[0], y[0], z[0]]) + inset
+    hi = np.array([x[-1], y[-1], z[-1]]) - inset
+    for _ in range(n_ell):
+        c = rng.uniform(lo, hi)
+        ax = rng.uniform(axes[0], axes[1], size=3)
+        R = haar_rotation(rng)
+        ev = float(cfg.sigma_b_at(c[2])) * 10.0 ** rng.uniform(-1.0, 1.0, size=3)
+        P = np.stack([X - c[0], Y - c[1], Z - c[2]], axis=-1) @ R
+        inside = np.sum((P / ax) ** 2, axis=-1) <= 1.0
+        s[inside] = R @ np.diag(ev) @ R.T
+    return s
+
+
 # ------------------------------------------------------------------------- c4 stations
 
 def c4_stations(n_stations=64, incl=70.0, azim=45.0, spacings=(1.0, 3.0, 7.0)):
@@ -223,6 +288,36 @@ def make_config(name):
                       boxes=box_grid((128, 128, 64), (4, 2, 1)), restart=30, outer_tol=1e-6,
                       note="homogeneous stand-in for the layered c4 at its middle-layer conductivity "
                            "(sigma_b = 0.01 S/m, 400 kHz): the slab and the trajectory sit in that layer")
+    lay3 = dict(layers=(1.0, 0.01, 1.0), z_iface=(-4.0, 4.0))
+    lay3mini = dict(layers=(1.0, 0.01, 1.0), z_iface=(-0.5, 0.5))
+    if name in ("c3", "c3capped"):
+        return Config(name, (64, 64, 64), 0.25, None, 4e5, 3, _c3_sigma if name == "c3" else _c3_sigma_capped,
+                      sources=[(np.zeros(3), tri[i]) for i in range(3)],
+                      receivers=[np.array([0.0, 0.0, z]) for z in (1.0, 3.0, 7.0)],
+                      boxes=box_grid((64, 64, 64), (2, 2, 1)), restart=30, outer_tol=1e-8, **lay3,
+                      note="three-layer background 1 / 0.01 / 1 S/m, interfaces at -4 / +4 m (physical table)")
+    if name in ("c3lmini", "c3lminicapped"):
+        fn = (lambda rng, c: _c3_sigma(rng, c, 4)) if name == "c3lmini" else (lambda rng, c: _c3_sigma_capped(rng, c, 4))
+        return Config(name, (8, 8, 8), 0.25, None, 4e5, 3, fn,
+                      sources=[(np.zeros(3), tri[i]) for i in range(3)],
+                      receivers=[np.array([0.0, 0.0, 1.0]), np.array([0.0, 0.0, -1.5])],
+                      boxes=box_grid((8, 8, 8), (2, 2, 1)), restart=30, outer_tol=1e-9, **lay3mini,
+                      note="c3 recipe on 8^3 with the interfaces scaled to -0.5 / +0.5 m")
+    if name == "c4":
+        st = c4_stations()
+        return Config(name, (128, 128, 64), 0.25, None, 4e5, 4, _c4_sigma_layered,
+                      sources=[(st[31]["tx"], st[31]["moments"][i]) for i in range(3)],
+                      receivers=list(st[31]["rx"]), rx_moments=tuple(map(tuple, st[31]["moments"])),
+                      boxes=box_grid((128, 128, 64), (4, 2, 1)), restart=30, outer_tol=1e-6, **lay3,
+                      note="three-layer background 1 / 0.01 / 1 S/m (physical table); station 31 of the sweep")
+    if name == "c4lmini":
+        F = tool_frame(70.0, 45.0)
+        tx = 0.1 * F[2]
+        return Config(name, (8, 8, 8), 0.25, None, 4e5, 4,
+                      lambda rng, c: _c4_sigma_layered(rng, c, slab_half=0.25, inset=0.5, n_ell=3, axes=(0.25, 0.5)),
+                      sources=[(tx, F[i]) for i in range(3)], receivers=[tx + 0.6 * F[2], tx + 1.2 * F[2]],
+                      rx_moments=tuple(map(tuple, F)), boxes=box_grid((8, 8, 8), (2, 2, 1)), restart=30,
+                      outer_tol=1e-9, **lay3mini, note="c4 recipe scaled to 8^3 (interfaces at -0.5 / +0.5 m)")
     if name == "c5":
         return Config(name, (256, 256, 128), 0.2, 0.5, 1e5, 5, _c5_sigma,
                       sources=[(np.zeros(3), zdip)],
@@ -235,4 +330,5 @@ def make_config(name):
     raise KeyError(name)
 
 
-CONFIG_NAMES = ("c1", "c2", "c2capped", "c2mod", "c2mini", "c3h", "c3mini", "c4h", "c5", "c5mini")
+CONFIG_NAMES = ("c1", "c2", "c2capped", "c2mod", "c2mini", "c3h", "c3mini", "c4h", "c5", "c5mini",
+                "c3", "c3capped", "c3lmini", "c3lminicapped", "c4", "c4lmini")

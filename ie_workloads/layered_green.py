@@ -578,6 +578,51 @@ def incident_E_layered(med, points, src, moments, rho_interp=True):
     return out
 
 
+def incident_E_layered_grid(med, x, y, z, src, moments):
+    """E0 on a tensor grid of cell centroids: (n_mom, 3, nz, ny, nx) complex128 -- the radial
+    functions are computed once per depth and interpolated to the (x, y) columns."""
+    x, y, z = (np.asarray(a, np.float64) for a in (x, y, z))
+    src = np.asarray(src, np.float64)
+    moments = np.atleast_2d(np.asarray(moments, np.float64))
+    m = int(med.layer_of(src[2]))
+    nx, ny, nz = len(x), len(y), len(z)
+    DX, DY = np.meshgrid(x - src[0], y - src[1], indexing="xy")  # (ny, nx)
+    rho = np.hypot(DX, DY).ravel()
+    lo = med.layer_of(z)
+    if med.L > 1:
+        dz = np.abs(z[:, None] - med.zi[None, :]).min()
+        ds = np.abs(src[2] - med.zi).min()
+        h_min = max(float(dz) + float(ds), 1e-4)
+    else:
+        h_min = 1.0
+    hseg = min(abs(x[1] - x[0]) if nx > 1 else 0.25, abs(y[1] - y[0]) if ny > 1 else 0.25)
+    out = np.zeros((len(moments), 3, nz, ny, nx), np.complex128)
+    iwm = 1j * med.omega * MU0
+    if med.L > 1 or m != 0:
+        nodes, segs = radial_nodes(max(float(rho.max()), hseg), hseg)
+        F = _mag_radial(med, z, src[2], nodes, h_min, m)  # (6, R, nz)
+        Lm = interp_matrix(segs, nodes, rho)  # (ny nx, R)
+        R = len(nodes)
+        Fr = F.transpose(1, 0, 2).reshape(R, -1)
+        Fp = (Lm @ Fr.real + 1j * (Lm @ Fr.imag)).reshape(ny, nx, 6, nz).transpose(2, 3, 0, 1)  # (6, nz, ny, nx)
+        c = np.where(rho > 0, DX.ravel() / np.where(rho > 0, rho, 1), 0.0).reshape(ny, nx)
+        s_ = np.where(rho > 0, DY.ravel() / np.where(rho > 0, rho, 1), 0.0).reshape(ny, nx)
+        c2, s2 = c * c - s_ * s_, 2 * s_ * c
+        F0a, F2a, F0b, F2b, F1c, F1e = Fp
+        for t, mm in enumerate(moments):
+            mx, my, mz = mm
+            out[t, 0] = iwm * (mx * (-F2a * s2 - F2b * s2) + my * (-F0a + F2a * c2 + F0b + F2b * c2) + mz * (-F1c * s_))
+            out[t, 1] = iwm * (mx * (F0a + F2a * c2 - F0b + F2b * c2) + my * (F2a * s2 + F2b * s2) + mz * (F1c * c))
+            out[t, 2] = iwm * (mx * (F1e * s_) - my * (F1e * c))
+    ks = np.where(lo == m)[0]
+    if len(ks):
+        Z, Y, X = np.meshgrid(z[ks], y, x, indexing="ij")
+        Rv = np.stack([X, Y, Z], axis=-1) - src
+        for t, mm in enumerate(moments):
+            out[t][:, ks] += np.moveaxis(_E_mag_hom(Rv, mm, med.wavenumber(m), med.omega), -1, 0)
+    return out
+
+
 def _mag_radial(med, zu, zs, rho, h_min, m, order=_GL_ORDER):
     """F (6, R, Z): F0(a), F2(a), F0(b), F2(b), F1(c), F1(e) for observer depths zu."""
     rmax = max(float(np.max(rho)), 1e-3)

@@ -115,6 +115,33 @@ class LayeredOperator:
         return E - self.scatter(E)
 
 
+def direct_rows_layered(Tq, dsigma, E, cells, identity=True):
+    """(I - G dsigma) E at output cells (ix, iy, iz) by the literal sum over every source cell
+    with the (mirror-expanded) table, R17: O(N) per output cell, any grid size."""
+    _, _, nz, _, ny, nx = Tq.shape
+    J = np.einsum("zyxpq,qzyx->pzyx", dsigma, E)  # (3, nz, ny, nx)
+    sx = np.outer(SX, SX)
+    sy = np.outer(SY, SY)
+    out = np.zeros((len(cells), 3), np.complex128)
+    ii = np.arange(nx)
+    jj = np.arange(ny)
+    for t, (cx, cy, cz) in enumerate(cells):
+        di = cx - ii  # (nx,) offsets observer - source
+        dj = cy - jj
+        # T_pq(di, dj; cz, k') for all sources, by the mirror rules of R18
+        Tk = Tq[:, :, cz]  # (3, 3, nz, ny, nx)
+        A = Tk[:, :, :, np.abs(dj)[:, None], np.abs(di)[None, :]]  # (3, 3, nz, ny, nx)
+        fx = np.where(di < 0, 1.0, 0.0)[None, None, None, None, :]
+        fy = np.where(dj < 0, 1.0, 0.0)[None, None, None, :, None]
+        A = A * np.where(fx > 0, sx[:, :, None, None, None], 1.0) * np.where(fy > 0, sy[:, :, None, None, None], 1.0)
+        # odd components vanish at zero offset (R18)
+        A = A * np.where((di == 0)[None, None, None, None, :], (sx > 0)[:, :, None, None, None], 1.0)
+        A = A * np.where((dj == 0)[None, None, None, :, None], (sy > 0)[:, :, None, None, None], 1.0)
+        s = np.einsum("pqzyx,qzyx->p", A, J)
+        out[t] = (E[:, cz, cy, cx] if identity else 0.0) - s
+    return out
+
+
 def box_table(Tq, box):
     """The table of the diagonal block of box (i0,i1,j0,j1,k0,k1): offsets below its
     extents and layer indices inside its z-range (Eq. 15 for the layered kernel)."""

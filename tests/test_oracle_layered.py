@@ -153,3 +153,33 @@ def test_spectrum_mirror_relation_on_arbitrary_tables():
         a = M[..., (2 * ny - iy) % (2 * ny), ix]
         b = np.einsum("p,q,pqkl->pqkl", lay.SY, lay.SY, M[..., iy, ix])
         assert np.abs(a - b).max() < 1e-15 * np.abs(M).max()
+
+
+def test_direct_rows_layered_equal_dense_assembly():
+    n = (5, 4, 3)
+    rng = np.random.default_rng(21)
+    Tq = lay.random_table(n, rng)
+    ds = _dsig(rng, n, 0.3)
+    E = _field(rng, n)
+    y = (lay.dense_matrix_layered(Tq, ds) @ E.ravel()).reshape(E.shape)
+    cells = [(0, 0, 0), (4, 3, 2), (2, 1, 1), (3, 0, 2)]
+    yd = lay.direct_rows_layered(Tq, ds, E, cells)
+    for t, (x, yy, z) in enumerate(cells):
+        assert np.abs(yd[t] - y[:, z, yy, x]).max() < 1e-13 * np.abs(y).max()
+
+
+@pytest.mark.parametrize("scheme", ["jacobi", "gauss_seidel"])
+def test_physical_layered_dd_converges_to_dense_lu(scheme):
+    """The c4 recipe on 8^3 with the physical three-layer table (layered_green): Algorithm 1
+    (2 x 2 boxes in x, y) reaches the dense LU solution, with E0 of the layered background."""
+    from ie_workloads import make_config, layered_inputs as li
+    cfg = make_config("c4lmini")
+    med = li.medium(cfg)
+    Tq = li.table(cfg, med)
+    sbz = lay.background_per_layer(cfg.n, cfg.origin, cfg.hvec, *cfg.background())
+    ds = lay.contrast_layered(cfg.sigma(), sbz)
+    E0 = li.incident(cfg, med)[0]
+    X = np.linalg.solve(lay.dense_matrix_layered(Tq, ds), E0.ravel()).reshape(E0.shape)
+    E, st = dd.solve_dd(lay.LayeredDDSystem(Tq, ds, cfg.boxes), E0, scheme, outer_tol=1e-11, restart=30)
+    assert st["converged"]
+    assert np.linalg.norm(E - X) < 1e-8 * np.linalg.norm(X)
