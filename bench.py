@@ -161,6 +161,44 @@ def replica_value(bytes_per_step, steps, t_ms_max, ws):
     return ws * bytes_per_step * steps / (t_ms_max / 1e3) / 1e9
 
 
+def sweep_units(stations, freqs):
+    """The independent systems of a logging sweep: one (frequency, station) pair each, in
+    frequency-major order (positions and frequencies are independent)."""
+    return [(float(f), int(s)) for f in freqs for s in stations]
+
+
+def rank_units(units, rank, ws):
+    """Contiguous share of the units for this rank (frequency-major order keeps the number of
+    distinct frequencies -- i.e. of per-frequency tables and contexts -- per rank minimal)."""
+    n = len(units)
+    return units[rank * n // ws:(rank + 1) * n // ws]
+
+
+def gather_results(local, ws):
+    """Merge every rank's {unit: result} on all ranks (torch.distributed.all_gather_object over
+    the process group: NCCL on GPUs, gloo in the CPU tests); a unit solved twice is an error."""
+    if ws <= 1:
+        return dict(local)
+    import torch.distributed as dist
+    objs = [None] * ws
+    dist.all_gather_object(objs, dict(local))
+    merged = {}
+    for o in objs:
+        for k, v in o.items():
+            assert k not in merged, f"unit {k} solved on two ranks"
+            merged[k] = v
+    return merged
+
+
+def distributed_sweep(units, solve, rank, ws):
+    """Replicas over the sweep's systems: this rank solves its share with
+    solve(unit) -> result (any picklable value); returns (merged results of all ranks, this
+    rank's units).  No data-path collective: the units share nothing."""
+    mine = rank_units(units, rank, ws)
+    local = {u: solve(u) for u in mine}
+    return gather_results(local, ws), mine
+
+
 def barrier(ws):
     if ws > 1:
         import torch.distributed as dist
@@ -168,61 +206,112 @@ def barrier(ws):
 
 
 # ----------------------------------------------------------------------------- oracle
-def oracle_sample_step(cfg, sigma, box):
-    """One oracle operator application (Eq. 8/10, numpy FFTs) on a sub-box of the workload."""
+def cpu_info():
+    """Host cores this process may use and the CPU model (/proc/cpuinfo)."""
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    model = None
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return cores, model
+
+
+def oracle_operator(cfg, sigma):
+    """The oracle's operator (Eq. 8/10, scipy.fft with workers = all affinity cores) on the
+    FULL workload grid; the Green-spectrum setup is not timed."""
     from oracle import physics, operator as op
-    i0, i1, j0, j1, k0_, k1 = box
-    n = (i1 - i0, j1 - j0, k1 - k0_)
     k0 = physics.wavenumber(cfg.sigma_b, cfg.freq)
-    ds = physics.contrast(sigma[k0_:k1, j0:j1, i0:i1], cfg.sigma_b)
-    A = op.Operator(n, cfg.hvec, k0, cfg.sigma_b, ds)  # setup (Green spectrum) not timed
+    ds = physics.contrast(sigma, cfg.sigma_b)
+    A = op.Operator(cfg.n, cfg.hvec, k0, cfg.sigma_b, ds)
+    nx, ny, nz = cfg.n
     rng = np.random.default_rng(0)
-    x = rng.standard_normal((3, n[2], n[1], n[0])) + 1j * rng.standard_normal((3, n[2], n[1], n[0]))
-    return A, x, n
+    x = rng.standard_normal((3, nz, ny, nx)) + 1j * rng.standard_normal((3, nz, ny, nx))
+    return A, x
+
+
+def time_oracle_apply(A, x, steps, warmup):
+    for _ in range(warmup):
+        A(x)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        A(x)
+    return (time.perf_counter() - t0) / steps
+
+
+def oracle_baseline_record(cfg, dt, steps):
+    cores, model = cpu_info()
+    from oracle._threads import WORKERS
+    nx, ny, nz = cfg.n
+    rec = {"value": b_model(nx, ny, nz) / dt / 1e9, "unit": "GB/s", "cores": WORKERS, "kind": "oracle",
+           "cpu_model": model, "affinity_cores": cores, "ms_per_apply": round(dt * 1e3, 1),
+           "sample": f"{steps} oracle applications of (I - G dsigma) on the FULL {cfg.name} grid "
+                     f"({nx}x{ny}x{nz}; numpy einsum + scipy.fft with workers={WORKERS}); same config as the "
+                     f"GPU line (same_config: true); Green-spectrum setup untimed"}
+    solves = os.path.join(ROOT, "profiles", "r02_oracle_solves.json")
+    if os.path.exists(solves):
+        rec["solves_committed"] = {"file": "profiles/r02_oracle_solves.json",
+                                   "note": "oracle solve timings measured by tools/oracle_baseline.py on a GPU box "
+                                           "host (not in this run: a c5 oracle solve takes minutes)"}
+    return rec
 
 
 def run_reference(args, cfg, sigma, rank, ws):
-    """--impl reference: the CPU oracle, as it stands, on bounded samples of the same workload."""
+    """--impl reference: the CPU oracle, as it stands, on the same workload (full c5 grid), the
+    same metric (B_model GB/s of one operator application)."""
     if rank != 0:
         return None
-    box = (0, 64, 0, 64, 0, 128) if cfg.name == "c5" else (0,) + (min(cfg.n[0], 64),) + (0, min(cfg.n[1], 64), 0,
-                                                                                       min(cfg.n[2], 128))
-    A, x, n = oracle_sample_step(cfg, sigma, box)
-    for _ in range(args.warmup):
-        A(x)
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        A(x)
-    dt = (time.perf_counter() - t0) / args.steps
-    v = b_model(*n) / dt / 1e9
+    A, x = oracle_operator(cfg, sigma)
+    dt = time_oracle_apply(A, x, args.steps, args.warmup)
+    rec = oracle_baseline_record(cfg, dt, args.steps)
+    v = rec["value"]
+    nx, ny, nz = cfg.n
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "GB/s", "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "c128", "data": "synthetic",
-            "config": {"workload": cfg.name, "sample_box": list(box), "grid": list(cfg.n)},
-            "cpu_baseline": {"value": v, "unit": "GB/s", "cores": 1, "kind": "oracle",
-                             "sample": f"one numpy-FFT operator application (Eq. 10) on the {n[0]}x{n[1]}x{n[2]} "
-                                       f"sub-box of {cfg.name} per step (single-threaded numpy)"},
+            "config": {"workload": cfg.name, "grid": [nx, ny, nz], "same_config": True},
+            "cpu_baseline": rec,
             "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     return line
 
 
 # ------------------------------------------------------------------------------- ours
-def layered_leg(steps=10, name="c3h", nrhs=3):
-    """A3L: the c3 grid (64^3) and its contrast recipe through the layered-table path (K-C'
-    z-z' contraction on the FP64 tensor cores) with the library's degenerate equal-layer table
-    (table_format 2, sigma = 1 S/m, 400 kHz -- the physical 3-layer table is not built, DESIGN
-    R19), triaxial source = 3 right-hand sides.  Per-kernel CUDA-event times."""
+def _layered_ctx(cfg, T, sigma_dev, nrhs, boxes, restart, freq=None):
+    import paper_2306_17537_b200 as ie
+    lay, zi = cfg.background()
+    ctx = ie.ie_create(cfg.n, cfg.hvec, cfg.origin, list(lay), cfg.freq if freq is None else freq, table=T,
+                       z_iface=list(zi))
+    ie.ensure_workspace(ctx, boxes=boxes, nrhs=nrhs, restart=restart)
+    ie.ie_set_contrast(ctx, sigma_dev)
+    return ctx
+
+
+def layered_leg(steps=10, name="c3"):
+    """A3L on the layered c3 (BASELINE.json configs[2]: 64^3, three layers 1 / 0.01 / 1 S/m,
+    400 kHz) with the PHYSICAL table (ie_workloads.layered_green, host input data): triaxial
+    source = 3 right-hand sides, operator applications with per-kernel CUDA-event times; the K-C'
+    z-z' contraction runs on the FP64 tensor cores (DMMA).  Host generation times reported apart."""
     import torch
     import paper_2306_17537_b200 as ie
-    from ie_workloads import make_config
+    from ie_workloads import make_config, layered_inputs as li
     cfg = make_config(name)
-    ctx = ie.ie_create(cfg.n, cfg.hvec, cfg.origin, cfg.sigma_b, cfg.freq, table_format=2)
-    ie.ensure_workspace(ctx, nrhs=nrhs, restart=2)
-    ie.ie_set_contrast(ctx, torch.from_numpy(cfg.sigma()).cuda())
-    ie.ie_set_source(ctx, np.array([s for s, _ in cfg.sources]), np.array([m for _, m in cfg.sources]))
+    t0 = time.perf_counter()
+    med = li.medium(cfg)
+    T = li.table(cfg, med)
+    t_table = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    E0 = li.incident(cfg, med)
+    t_e0 = time.perf_counter() - t0
+    nrhs = len(E0)
+    t0 = time.perf_counter()
+    ctx = _layered_ctx(cfg, T, torch.from_numpy(cfg.sigma()).cuda(), nrhs, [], 2)
+    torch.cuda.synchronize()
+    t_setup = time.perf_counter() - t0
     nx, ny, nz = cfg.n
-    x = torch.empty((nrhs, 3, nz, ny, nx), dtype=torch.complex128, device="cuda")
-    ie.ie_get_incident(ctx, x)
+    x = torch.from_numpy(E0).cuda()
     y = torch.empty_like(x)
     for _ in range(3):
         ie.ie_apply_operator(ctx, x, y)
@@ -243,10 +332,220 @@ def layered_leg(steps=10, name="c3h", nrhs=3):
     table = (nx + 1) * (ny + 1) * R * R * 16
     x2 = 2 * nrhs * 12 * nx * ny * nz * 16
     flops = 8 * R * R * 4 * nx * ny * nrhs
-    return {"workload": f"{name} grid, degenerate table (format 2), {nrhs} RHS", "ms_per_apply": round(ms, 4),
+    return {"workload": f"{name} (64^3, layers 1/0.01/1 S/m at -4/+4 m, physical table), {nrhs} RHS",
+            "ms_per_apply": round(ms, 4),
             "kernels_ms": {k: round(v[0] / max(1, v[1]), 4) for k, v in prof.items()},
             "k_c_prime": {"ms": round(kc_ms, 4), "alg_bytes": table + x2, "gbs": round((table + x2) / kc_ms / 1e6, 1),
-                          "fp64_tflops": round(flops / kc_ms / 1e9, 2), "pipe": "DMMA m8n8k4 f64 (tensor cores)"}}
+                          "fp64_tflops": round(flops / kc_ms / 1e9, 2), "pipe": "DMMA m8n8k4 f64 (tensor cores)"},
+            "host_generation_s": {"table": round(t_table, 2), "incident": round(t_e0, 2)},
+            "setup_s": round(t_setup, 3)}
+
+
+def _layered_position(ctx, E0h, e0rxh, h0, scheme, boxes, outer_tol, restart, precond, adaptive=True):
+    """One tool position on a layered context: H2D of the host-generated E0 and receiver-dipole
+    E0, Algorithm 1 (or full GMRES), receiver couplings by reciprocity.  Device-timed."""
+    import torch
+    import paper_2306_17537_b200 as ie
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    ev0.record()
+    E0 = E0h.cuda(non_blocking=True)
+    e0rx = e0rxh.cuda(non_blocking=True)
+    ie.ie_set_incident(ctx, E0)
+    e = torch.empty_like(E0)
+    st = ie.ie_solve_dd(ctx, e, scheme, boxes=boxes, outer_tol=outer_tol, adaptive=adaptive, restart=restart,
+                        inner_tol_fixed=1e-2 if scheme.startswith("fgmres") else 1e-6,
+                        max_sweeps=100, max_iters=3000, check=False, precond=precond)
+    H = ie.ie_receiver_fields_table(ctx, e, e0rx, h0)
+    ev1.record()
+    torch.cuda.synchronize()
+    return ev0.elapsed_time(ev1) / 1e3, st, H
+
+
+DD_KEYS = {"full": "full_gmres", "jacobi": "jacobi_a", "gauss_seidel": "gs_a", "fgmres_jacobi": "jacobi_fgmres",
+           "fgmres_gauss_seidel": "gs_fgmres"}
+
+
+def layered_dd_leg(name="c3capped", runs=(("full", 0), ("gauss_seidel", 0), ("jacobi", 0), ("full", 1),
+                                          ("gauss_seidel", 1), ("jacobi", 1)), reps=1):
+    """Forward solve seconds per tool position on a layered config (c3 recipe: triaxial source =
+    3 RHS, 2x2 boxes, receivers at 1/3/7 m x 3 axes by reciprocity), per scheme; generation of
+    the host inputs (table, E0, receiver-dipole E0) timed apart."""
+    import torch
+    import paper_2306_17537_b200 as ie
+    from ie_workloads import make_config, layered_inputs as li
+    cfg = make_config(name)
+    g0 = time.perf_counter()
+    med = li.medium(cfg)
+    T = li.table(cfg, med)
+    g1 = time.perf_counter()
+    E0 = torch.from_numpy(li.incident(cfg, med)).pin_memory()
+    e0rx, h0 = li.receiver_inputs(cfg, med)
+    e0rx = torch.from_numpy(e0rx).pin_memory()
+    g2 = time.perf_counter()
+    t0 = time.perf_counter()
+    ctx = _layered_ctx(cfg, T, torch.from_numpy(cfg.sigma()).cuda(), len(E0), cfg.boxes, cfg.restart)
+    torch.cuda.synchronize()
+    out = {"workload": f"{name}: {cfg.note}; {len(E0)} RHS, {len(cfg.boxes)} boxes, outer tol {cfg.outer_tol}",
+           "host_generation_s": {"table": round(g1 - g0, 2), "incident_and_receivers": round(g2 - g1, 2)},
+           "setup_s": round(time.perf_counter() - t0, 3),
+           "position": "H2D of E0 + receiver-dipole E0, solve, receiver couplings (device-timed)"}
+    for scheme, pc in runs:
+        times, st = [], None
+        for rep in range(1 + reps):
+            t, st, H = _layered_position(ctx, E0, e0rx, h0, scheme, cfg.boxes, cfg.outer_tol, cfg.restart, pc)
+            if rep > 0 or reps == 0:
+                times.append(t)
+        status = ie.STATUS.get(st["status"], st["status"])
+        key = DD_KEYS[scheme] + ("_cie" if pc else "")
+        out[key] = {"s_per_position": float(np.median(times)) if status == "IE_OK" else None,
+                    "s_measured": float(np.median(times)), "sweeps": st["sweeps"],
+                    "gmres_iters": st["total_inner_iters"], "full_applies": st["full_applies"],
+                    "sub_applies": st["sub_applies"], "e_final": st["e_final"], "status": status}
+    return out
+
+
+def c4_layered_units(units, runs=(("full", 1), ("gauss_seidel", 1)), verbose=False, name="c4", outer_tol=None):
+    """Solve (frequency, station) units of the c4 deviated-well sweep (BASELINE.json configs[3])
+    on the three-layer background.  Per frequency one context: the physical table is generated on
+    the host and uploaded once, the layered spectra are amortised over the stations (excluded from
+    s/position).  Per unit the host generates the layered E0 of the triaxial
+    transmitter and of the 9 receiver dipoles (1/3/7 m x tool axes) -- overlapped with the
+    previous unit's GPU work and reported apart -- and the GPU runs H2D + solve + receiver
+    couplings (device-timed).  Returns ({unit: {run: [s, iters, status]}}, info)."""
+    import concurrent.futures as cf
+    import torch
+    import paper_2306_17537_b200 as ie
+    from ie_workloads import make_config, layered_inputs as li
+    from ie_workloads.configs import c4_stations
+    cfg = make_config(name)
+    tol = cfg.outer_tol if outer_tol is None else outer_tol
+    sigma = torch.from_numpy(cfg.sigma()).cuda()
+    st_all = c4_stations()
+    info = {"table_s": {}, "setup_s": {}, "gen_s": []}
+    res = {}
+    pool = cf.ThreadPoolExecutor(1)
+
+    def gen(med, s):
+        t0 = time.perf_counter()
+        srcs = [(st_all[s]["tx"], m) for m in st_all[s]["moments"]]
+        E0 = torch.from_numpy(li.incident(cfg, med, srcs)).pin_memory()
+        e0rx, h0 = li.receiver_inputs(cfg, med, srcs, st_all[s]["rx"])
+        return E0, torch.from_numpy(e0rx).pin_memory(), h0, time.perf_counter() - t0
+
+    for f in sorted({u[0] for u in units}, key=lambda v: [u[0] for u in units].index(v)):
+        mine = [u for u in units if u[0] == f]
+        t0 = time.perf_counter()
+        med = li.medium(cfg, f)
+        T = li.table(cfg, med)
+        info["table_s"][str(f)] = round(time.perf_counter() - t0, 2)
+        t0 = time.perf_counter()
+        ctx = _layered_ctx(cfg, T, sigma, 3, cfg.boxes, cfg.restart, freq=f)
+        torch.cuda.synchronize()
+        info["setup_s"][str(f)] = round(time.perf_counter() - t0, 3)
+        del T
+        fut = pool.submit(gen, med, mine[0][1])
+        for i, u in enumerate(mine):
+            E0, e0rx, h0, g = fut.result()
+            info["gen_s"].append(g)
+            if i + 1 < len(mine):
+                fut = pool.submit(gen, med, mine[i + 1][1])
+            res[u] = {}
+            for scheme, pc in runs:
+                t, st, H = _layered_position(ctx, E0, e0rx, h0, scheme, cfg.boxes, tol, cfg.restart, pc)
+                k = DD_KEYS[scheme] + ("_cie" if pc else "")
+                res[u][k] = [t, st["total_inner_iters"], ie.STATUS.get(st["status"], st["status"])]
+                if verbose:
+                    print(f, u[1], k, round(t, 4), st["total_inner_iters"], st["sweeps"], st["e_final"], flush=True)
+        del ctx
+        torch.cuda.empty_cache()
+    pool.shutdown()
+    return res, info
+
+
+def c4_layered_sweep(stations=(0, 31, 63), freqs=(4e5,), runs=(("full", 1), ("gauss_seidel", 1)), verbose=False,
+                     rank=0, ws=1, name="c4", outer_tol=None):
+    """The c4 sweep summary: s/position per scheme (sum over frequencies of one station's device
+    time, mean over stations).  With ws > 1 ranks the (frequency, station) units are split
+    between the ranks (replicas, no data-path collective) and the aggregate s/position is the
+    slowest rank's total device time over the number of stations."""
+    units = sweep_units(stations, freqs)
+    mine = rank_units(units, rank, ws)
+    t0 = time.perf_counter()
+    res, info = c4_layered_units(mine, runs, verbose, name, outer_tol) if mine else ({}, {"table_s": {}, "setup_s": {}, "gen_s": []})
+    wall = time.perf_counter() - t0
+    merged = gather_results(res, ws)
+    infos = gather_results({rank: info}, ws)
+    out = {"workload": f"{name} sweep (128x128x64, layers 1/0.01/1 S/m, triaxial, rx 1/3/7 m x 3 axes)",
+           "outer_tol": outer_tol,
+           "stations": list(stations), "freqs": list(freqs), "n_ranks": ws, "units": len(units),
+           "table_s": {r: v["table_s"] for r, v in infos.items()}, "setup_s": {r: v["setup_s"] for r, v in infos.items()},
+           "generation_s_per_unit": round(float(np.mean([g for v in infos.values() for g in v["gen_s"]])), 2),
+           "rank_wall_s": round(wall, 2)}
+    for scheme, pc in runs:
+        k = DD_KEYS[scheme] + ("_cie" if pc else "")
+        by_station = {}
+        for (f, s), r in merged.items():
+            by_station[s] = by_station.get(s, 0.0) + r[k][0]
+        rank_time = {}
+        for r in range(ws):
+            rank_time[r] = sum(merged[u][k][0] for u in rank_units(units, r, ws))
+        out[k] = {"s_per_position": round(float(np.mean(list(by_station.values()))), 4),
+                  "per_station_s": {str(s): round(t, 4) for s, t in sorted(by_station.items())},
+                  "gmres_iters": [merged[u][k][1] for u in units], "status": sorted({merged[u][k][2] for u in units})}
+        if ws > 1:
+            out[k]["aggregate_s_per_position"] = round(max(rank_time.values()) / len(stations), 4)
+    return out
+
+
+def moving_window(n_stations=5, n=(256, 128, 128), h=0.25, splits=(2, 1, 1), scheme="gauss_seidel", tol=1e-3,
+                  precond=0, restart=50):
+    """The paper's moving-window logging simulation (section 3.3):
+    one context for the window geometry (Green spectrum once, sigma0 = 0.1 S/m constant per window,
+    P:281); per station the window conductivity is sampled from the analytic formation ON THE
+    DEVICE (ie_workloads.logging.window_sigma_device, rotated into the window frame, App. C), then
+    E0 of the axial transmitter, Algorithm 1 (GS-A, tol 1e-3 as P:285) over the sub-domains and
+    the receivers at 7/15/30 m.  s/position includes the sigma generation.  Window 1 of the paper:
+    128x128x256 cells, 2 sub-domains along the hole; window 2: 256^3 cells, 8 sub-domains."""
+    import torch
+    import paper_2306_17537_b200 as ie
+    from ie_workloads import logging as lg
+    from ie_workloads import box_grid
+    origin, _ = lg.window_grid(n, h)
+    nx, ny, nz = n
+    boxes = box_grid(n, splits)
+    t0 = time.perf_counter()
+    ctx = ie.ie_create(n, (h, h, h), origin, lg.SIGMA0, lg.FREQ)
+    ie.ensure_workspace(ctx, boxes=boxes, nrhs=1, restart=restart)
+    torch.cuda.synchronize()
+    setup = time.perf_counter() - t0
+    tx_w, m_w, rx_w = lg.tool_in_window()
+    e = torch.empty((1, 3, nz, ny, nx), dtype=torch.complex128, device="cuda")
+    rows = []
+    for tx in lg.stations(n_stations):
+        ev0, ev1, evg = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        torch.cuda.synchronize()
+        ev0.record()
+        sig = lg.window_sigma_device(tx, n, h)
+        evg.record()
+        ie.ie_set_contrast(ctx, sig)
+        ie.ie_set_source(ctx, tx_w[None], m_w[None])
+        st = ie.ie_solve_dd(ctx, e, scheme, boxes=boxes, outer_tol=tol, restart=restart, max_sweeps=30,
+                            max_iters=1500, check=False, precond=precond)
+        H, _ = ie.ie_receiver_fields(ctx, e, np.array(rx_w))
+        ev1.record()
+        torch.cuda.synchronize()
+        del sig
+        rows.append(dict(tx=[round(v, 3) for v in tx], s=round(ev0.elapsed_time(ev1) / 1e3, 4),
+                         gen_s=round(ev0.elapsed_time(evg) / 1e3, 4), sweeps=st["sweeps"],
+                         iters=st["total_inner_iters"], e=st["e_final"], status=ie.STATUS.get(st["status"]),
+                         Hax=[abs(H[0, r, 0]) for r in range(len(rx_w))]))
+    return {"workload": f"moving window {nx}x{ny}x{nz} cells of {h} m, {scheme}{'+CIE' if precond else ''}, "
+                        f"tol {tol}, {len(boxes)} sub-domains",
+            "setup_s": round(setup, 3), "s_per_position": round(float(np.mean([r["s"] for r in rows])), 4),
+            "generation_s_per_position": round(float(np.mean([r["gen_s"] for r in rows])), 4),
+            "generation": "window sigma sampled and rotated on the device (torch), included in s/position",
+            "stations": rows}
 
 
 C4_FREQS = (1e5, 4e5, 2e6)
@@ -468,16 +767,22 @@ def run_ours(args, cfg, sigma, rank, ws, local):
            "result_matches_device_apply": ok}
 
     cufft = None if args.no_cufft else cufft_reference(ctx, cfg, sigma, x)
-    layered = None if args.no_layered else layered_leg()
-    sweep = None if args.no_sweep else c4_sweep()
+    layered = None
+    if not args.no_layered:  # the layered configs c3 / c4 with the physical three-layer table
+        layered = {"operator_c3": layered_leg(),
+                   "dd_c3capped": layered_dd_leg("c3capped"),
+                   "dd_c3_literal": layered_dd_leg("c3", runs=(("full", 1), ("gauss_seidel", 1)), reps=0)}
+    sweep = None if args.no_sweep else c4_layered_sweep(rank=rank, ws=ws, freqs=C4_FREQS if ws > 1 else (4e5,))
     window = None
     if not args.no_window:  # the paper's moving-window logging (section 3.3)
-        sys.path.insert(0, os.path.join(ROOT, "tools"))
-        import logging_window
-        window = {sch: logging_window.run(3, scheme=sch) for sch in ("gauss_seidel", "full")}
-        for w in window.values():
-            w["paper_context"] = "window 1 (128x128x256 cells), GS-A tol 1e-3: ~1.5 min per position on an " \
-                                 "RTX 3060 Laptop with MATLAB (P:287)"
+        window = {"window1_" + sch: moving_window(3, scheme=sch) for sch in ("gauss_seidel", "full")}
+        window["window2_gauss_seidel"] = moving_window(2, n=(256, 256, 256), splits=(2, 2, 2))
+        window["window2_full"] = moving_window(2, n=(256, 256, 256), splits=(2, 2, 2), scheme="full")
+        for k, w in window.items():
+            w["paper_context"] = ("window 1 (128x128x256 cells, 2 sub-domains), GS-A tol 1e-3: ~1.5 min per position"
+                                  if k.startswith("window1") else
+                                  "window 2 (256^3 cells, 8 sub-domains), GS-A tol 1e-3: ~15 min per position") + \
+                " on an RTX 3060 Laptop with MATLAB (P:287)"
 
     # --- forward solve seconds per tool position (full-domain GMRES vs DD schemes)
     dd = None
@@ -541,7 +846,19 @@ def main():
     assert args.warmup >= 3 or args.impl == "reference" or args.warmup >= 0
 
     from ie_workloads import make_config
+    if args.gpus > 1 and int(os.environ.get("WORLD_SIZE", "1")) == 1:
+        # one process per GPU: relaunch under torchrun (rendezvous on 127.0.0.1)
+        import socket
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+        os.execv(sys.executable, cmd)
     rank, ws, local = dist_init()
+    assert ws == args.gpus, f"--gpus {args.gpus} but WORLD_SIZE {ws}"
+    if ws > 1:  # the scaling run: operator replicas + the distributed c4 sweep only
+        args.no_cufft = args.no_layered = args.no_dd = args.no_window = True
     cfg = make_config(args.config)
     sigma = cfg.sigma()
     if args.impl == "reference":
@@ -556,9 +873,9 @@ def main():
         return
     cpu = None
     if not args.no_cpu_baseline and ws == 1:
-        ref_args = argparse.Namespace(steps=2, warmup=1)
-        rl = run_reference(ref_args, cfg, sigma, 0, 1)
-        cpu = rl["cpu_baseline"]
+        A, xo = oracle_operator(cfg, sigma)
+        cpu = oracle_baseline_record(cfg, time_oracle_apply(A, xo, 2, 1), 2)
+        del A, xo
     nx, ny, nz = cfg.n
     line = {"metric": METRIC, "value": round(r["value"], 2), "unit": "GB/s", "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(r["per_step"], 4), "higher_is_better": True,

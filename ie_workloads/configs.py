@@ -202,12 +202,14 @@ def _c3_sigma_capped(rng, cfg, block=16):
     return 0.5 * (s + np.swapaxes(s, -1, -2))
 
 
-def _c4_sigma_layered(rng, cfg, slab_half=1.0, inset=2.0, n_ell=20, axes=(0.5, 2.0)):
+def _c4_sigma_layered(rng, cfg, slab_half=1.0, inset=2.0, n_ell=20, axes=(0.5, 2.0), slab_in_middle_only=False):
     """c4 (layered, BASELINE.json configs[3]): background sigma_b(z) of the three layers, then a
     slab of half-thickness 1 m through the origin with normal (sin30, 0, cos30), TI sigma_h = 0.02,
     sigma_v = 0.005 about the normal (App. C, theta = 30 deg, phi = 0); then 20 ellipsoids:
-    centre U over the grid inset 2 m, semi-axes U[0.5, 2] m, Haar rotation, eigenvalues
-    sigma_b(centre) 10^U[-1, 1]; later objects overwrite earlier ones."""
+    centre U over the grid inset 2 m, semi-axes U[0.5, 2] m, Haar rotation R, eigenvalue RATIOS
+    r = 10^U[-1, 1]; an ellipsoid cell takes sigma_b(z_cell) R diag(r) R^T, i.e. its contrast
+    to the local background stays in [-0.9, 9] even where it crosses an interface (DESIGN.md
+    R22; BASELINE.json leaves the inclusions' values open); later objects overwrite earlier ones."""
     nx, ny, nz = cfg.n
     z, y, x = (cfg.cell_centers(2), cfg.cell_centers(1), cfg.cell_centers(0))
     s = np.zeros((nz, ny, nx, 3, 3))
@@ -215,6 +217,8 @@ def _c4_sigma_layered(rng, cfg, slab_half=1.0, inset=2.0, n_ell=20, axes=(0.5, 2
     Z, Y, X = np.meshgrid(z, y, x, indexing="ij")
     nrm = np.array([np.sin(np.radians(30)), 0.0, np.cos(np.radians(30))])
     slab = np.abs(X * nrm[0] + Y * nrm[1] + Z * nrm[2]) <= slab_half
+    if slab_in_middle_only:  # c4mid: the slab ends at the interfaces (a bed of the middle layer)
+        slab &= cfg.sigma_b_at(Z) == min(cfg.layers)
     s[slab] = vti_tensor(0.02, 0.005, np.radians(30.0), 0.0)
     lo = np.array([x[0], y[0], z[0]]) + inset
     hi = np.array([x[-1], y[-1], z[-1]]) - inset
@@ -222,10 +226,10 @@ def _c4_sigma_layered(rng, cfg, slab_half=1.0, inset=2.0, n_ell=20, axes=(0.5, 2
         c = rng.uniform(lo, hi)
         ax = rng.uniform(axes[0], axes[1], size=3)
         R = haar_rotation(rng)
-        ev = float(cfg.sigma_b_at(c[2])) * 10.0 ** rng.uniform(-1.0, 1.0, size=3)
+        ratio = 10.0 ** rng.uniform(-1.0, 1.0, size=3)
         P = np.stack([X - c[0], Y - c[1], Z - c[2]], axis=-1) @ R
         inside = np.sum((P / ax) ** 2, axis=-1) <= 1.0
-        s[inside] = R @ np.diag(ev) @ R.T
+        s[inside] = cfg.sigma_b_at(Z[inside])[:, None, None] * (R @ np.diag(ratio) @ R.T)
     return s
 
 
@@ -310,6 +314,15 @@ def make_config(name):
                       receivers=list(st[31]["rx"]), rx_moments=tuple(map(tuple, st[31]["moments"])),
                       boxes=box_grid((128, 128, 64), (4, 2, 1)), restart=30, outer_tol=1e-6, **lay3,
                       note="three-layer background 1 / 0.01 / 1 S/m (physical table); station 31 of the sweep")
+    if name == "c4mid":
+        st = c4_stations()
+        return Config(name, (128, 128, 64), 0.25, None, 4e5, 4,
+                      lambda rng, c: _c4_sigma_layered(rng, c, slab_in_middle_only=True),
+                      sources=[(st[31]["tx"], st[31]["moments"][i]) for i in range(3)],
+                      receivers=list(st[31]["rx"]), rx_moments=tuple(map(tuple, st[31]["moments"])),
+                      boxes=box_grid((128, 128, 64), (4, 2, 1)), restart=30, outer_tol=1e-6, **lay3,
+                      note="c4 with the resistive slab confined to the middle layer (in the 1 S/m shoulders "
+                           "it is a 200x resistive sheet that stalls the DD iterations)")
     if name == "c4lmini":
         F = tool_frame(70.0, 45.0)
         tx = 0.1 * F[2]
@@ -331,4 +344,4 @@ def make_config(name):
 
 
 CONFIG_NAMES = ("c1", "c2", "c2capped", "c2mod", "c2mini", "c3h", "c3mini", "c4h", "c5", "c5mini",
-                "c3", "c3capped", "c3lmini", "c3lminicapped", "c4", "c4lmini")
+                "c3", "c3capped", "c3lmini", "c3lminicapped", "c4", "c4mid", "c4lmini")

@@ -105,3 +105,39 @@ def tool_in_window():
     """Transmitter at the window origin of the tool frame (0,0,0), moment along the hole axis
     (the window x axis); receivers ahead on the axis."""
     return (np.zeros(3), np.array([1.0, 0.0, 0.0]), [np.array([s, 0.0, 0.0]) for s in SPACINGS])
+
+
+def window_sigma_device(tx, n, h, behind=17.0, device="cuda"):
+    """window_sigma evaluated with torch on the device (the formation is an analytic function of
+    position, so a station's window needs no host work or H2D copy): the same recipe, the same
+    float64 arithmetic, returned as a (nz, ny, nx, 3, 3) float64 tensor on `device`.  Input
+    generation only (torch elementwise ops), like the numpy version."""
+    import torch
+    origin, R = window_grid(n, h, behind)
+    nx, ny, nz = n
+    f64 = dict(dtype=torch.float64, device=device)
+    Rt = torch.tensor(R, **f64)
+    z = origin[2] + h * torch.arange(nz, **f64)
+    y = origin[1] + h * torch.arange(ny, **f64)
+    x = origin[0] + h * torch.arange(nx, **f64)
+    Z, Y, X = torch.meshgrid(z, y, x, indexing="ij")
+    local = torch.stack([X, Y, Z], dim=-1)
+    glob = torch.tensor(np.asarray(tx, np.float64), **f64) + local @ Rt.T
+    gx, gz = glob[..., 0], glob[..., 2]
+    shift = gx * np.tan(np.radians(DIP_DEG)) + torch.where(gx > FAULT_X, -FAULT_THROW, 0.0)
+    zr = gz - shift
+    d = np.radians(DIP_DEG)
+    nvec = torch.tensor([-np.sin(d), 0.0, np.cos(d)], **f64)
+    nn = torch.outer(nvec, nvec)
+    eye = torch.eye(3, **f64)
+    pert = 1.0 + ALPHA * torch.exp(-torch.linalg.vector_norm(glob - torch.tensor(R_C, **f64), dim=-1) / GAMMA)
+    s = torch.zeros(glob.shape[:-1] + (3, 3), **f64)
+    for i, (top, kind, a, b) in enumerate(BEDS):
+        bottom = BEDS[i + 1][0] if i + 1 < len(BEDS) else -1e9
+        m = ((zr < top) & (zr >= bottom))[..., None, None]
+        if kind == "shale":
+            val = (a * eye + (b - a) * nn).expand_as(s)
+        else:
+            val = (a * pert)[..., None, None] * eye
+        s = torch.where(m, val, s)
+    return torch.einsum("ia,...ij,jb->...ab", Rt, s, Rt).contiguous()

@@ -30,6 +30,9 @@ T = K(di, dj, k - k') of operator.py; pins the machinery against Eq. 10) and
 """
 
 import numpy as np
+import scipy.fft as sfft
+
+from ._threads import WORKERS
 
 from . import physics
 
@@ -85,7 +88,7 @@ def layered_spectra(Tq):
     dj = np.arange(-(ny - 1), ny) % (2 * ny)
     di = np.arange(-(nx - 1), nx) % (2 * nx)
     C[..., dj[:, None], di[None, :]] = F
-    return np.fft.fft2(C, axes=(4, 5))
+    return sfft.fft2(C, axes=(4, 5), workers=WORKERS)
 
 
 def layered_scatter(Mhat, dsigma, E):
@@ -95,9 +98,9 @@ def layered_scatter(Mhat, dsigma, E):
     J = np.einsum("zyxpq,qzyx->pzyx", dsigma, E)
     Jp = np.zeros((3, nz, 2 * ny, 2 * nx), np.complex128)
     Jp[:, :, :ny, :nx] = J
-    Jh = np.fft.fft2(Jp, axes=(2, 3))
+    Jh = sfft.fft2(Jp, axes=(2, 3), workers=WORKERS)
     Yh = np.einsum("pqkluv,qluv->pkuv", Mhat, Jh)
-    return np.fft.ifft2(Yh, axes=(2, 3))[:, :, :ny, :nx]
+    return sfft.ifft2(Yh, axes=(2, 3), workers=WORKERS)[:, :, :ny, :nx]
 
 
 class LayeredOperator:

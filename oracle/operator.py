@@ -12,6 +12,9 @@ Field layout (3, nz, ny, nx); dsigma layout (nz, ny, nx, 3, 3).
 """
 
 import numpy as np
+import scipy.fft as sfft
+
+from ._threads import WORKERS
 
 from . import physics
 
@@ -75,7 +78,7 @@ def green_spectra(n, h, k0, sigma_b):
     dy = np.arange(-(ny - 1), ny) % (2 * ny)
     dx = np.arange(-(nx - 1), nx) % (2 * nx)
     C[:, :, dz[:, None, None], dy[None, :, None], dx[None, None, :]] = K.transpose(3, 4, 0, 1, 2)
-    return np.fft.fftn(C, axes=(2, 3, 4))
+    return sfft.fftn(C, axes=(2, 3, 4), workers=WORKERS)
 
 
 def fft_scatter(Ghat, dsigma, E, n):
@@ -85,9 +88,9 @@ def fft_scatter(Ghat, dsigma, E, n):
     J = contrast_source(dsigma, E)
     Jp = np.zeros((3, 2 * nz, 2 * ny, 2 * nx), np.complex128)
     Jp[:, :nz, :ny, :nx] = J
-    Jh = np.fft.fftn(Jp, axes=(1, 2, 3))
+    Jh = sfft.fftn(Jp, axes=(1, 2, 3), workers=WORKERS)
     Yh = np.einsum("pqzyx,qzyx->pzyx", Ghat, Jh)
-    Y = np.fft.ifftn(Yh, axes=(1, 2, 3))
+    Y = sfft.ifftn(Yh, axes=(1, 2, 3), workers=WORKERS)
     return Y[:, :nz, :ny, :nx]
 
 

@@ -1,0 +1,84 @@
+"""Full-size c5 parity against the oracle (256x256x128 cells, 25 M complex128 unknowns; BASELINE
+north_star: operator to rel-L2 <= 1e-12, fields and receiver voltages <= 1e-6 at solver tol 1e-9).
+
+* the operator, element by element over the whole grid, vs the oracle's Eq. 10 FFT convolution
+  (oracle.operator.Operator, scipy.fft on all host cores);
+* the solves: the oracle's restarted GMRES with the contraction-IE right preconditioner
+  (oracle/preconditioner.py, pinned) to 1e-12 is the truth; the GPU's full-domain GMRES, GS-A and
+  FGMRES-Jacobi at tol 1e-9 must match it in the fields and receiver H / voltages, and DD must
+  agree with the full-domain solve (section 3.1).
+Marked slow: the oracle solve takes several minutes on the box's host cores."""
+
+import numpy as np
+import pytest
+
+from ie_workloads import make_config
+from oracle import physics, operator as op, gmres, preconditioner as pc, receivers
+from gpu_helpers import gpu_ctx, rel
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+
+@pytest.fixture(scope="module")
+def c5():
+    cfg = make_config("c5")
+    sigma = cfg.sigma()
+    k0 = physics.wavenumber(cfg.sigma_b, cfg.freq)
+    ds = physics.contrast(sigma, cfg.sigma_b)
+    A = op.Operator(cfg.n, cfg.hvec, k0, cfg.sigma_b, ds)
+    return cfg, sigma, k0, ds, A
+
+
+def test_c5_operator_elementwise(c5):
+    import torch
+    import paper_2306_17537_b200 as ie
+    cfg, sigma, k0, ds, A = c5
+    nx, ny, nz = cfg.n
+    ctx, _ = gpu_ctx(cfg, sigma=sigma, boxes=[], nrhs=1, restart=2)
+    g = torch.Generator(device="cuda").manual_seed(11)
+    x = torch.randn((1, 3, nz, ny, nx), dtype=torch.complex128, device="cuda", generator=g)
+    y = torch.empty_like(x)
+    ie.ie_apply_operator(ctx, x, y)
+    ref = A(x.cpu().numpy()[0])
+    assert rel(y.cpu().numpy()[0], ref) < 1e-12
+
+
+@pytest.fixture(scope="module")
+def c5_truth(c5):
+    """Oracle solution at tol 1e-12 (contraction-IE right-preconditioned GMRES: same system, same
+    Eq. 9 residual) and its receiver fields."""
+    cfg, sigma, k0, ds, A = c5
+    pts = physics.centroids(cfg.n, cfg.hvec, cfg.origin)
+    src, m = cfg.sources[0]
+    E0 = np.ascontiguousarray(np.moveaxis(physics.incident_E(pts, src, m, k0, cfg.freq), -1, 0))
+    del pts
+    P = pc.contraction_P(sigma, cfg.sigma_b)
+    chi, info = gmres.gmres(lambda c: A(pc.apply_cellwise(P, c)), E0, tol=1e-12, restart=30, max_iters=400)
+    assert info["converged"], info["relres_true"]
+    E = pc.apply_cellwise(P, chi)
+    H = receivers.receiver_H(cfg.n, cfg.hvec, cfg.origin, k0, cfg.sigma_b, ds, E, cfg.receivers, src, m)
+    return E0, E, H, info
+
+
+@pytest.mark.parametrize("scheme,precond", [("full", 0), ("full", 1), ("gauss_seidel", 1), ("fgmres_jacobi", 1)])
+def test_c5_solves_match_the_oracle(c5, c5_truth, scheme, precond):
+    import torch
+    import paper_2306_17537_b200 as ie
+    cfg, sigma, k0, ds, A = c5
+    E0, E_ref, H_ref, _ = c5_truth
+    ctx, _ = gpu_ctx(cfg, sigma=sigma)
+    nx, ny, nz = cfg.n
+    e0 = torch.empty((1, 3, nz, ny, nx), dtype=torch.complex128, device="cuda")
+    ie.ie_get_incident(ctx, e0)
+    assert rel(e0.cpu().numpy()[0], E0) < 1e-12  # A10 at full size
+    e = torch.empty_like(e0)
+    st = ie.ie_solve_dd(ctx, e, scheme, boxes=cfg.boxes, outer_tol=1e-9, restart=cfg.restart, max_sweeps=200,
+                        max_iters=3000, precond=precond,
+                        inner_tol_fixed=1e-2 if scheme.startswith("fgmres") else 1e-6)
+    assert st["e_final"] <= 1e-9
+    assert rel(e.cpu().numpy()[0], E_ref) < 1e-6
+    H, V = ie.ie_receiver_fields(ctx, e, np.array(cfg.receivers))
+    assert rel(H[0], H_ref) < 1e-6
+    m_r = np.eye(3)
+    V_ref = np.stack([receivers.voltage(H_ref, m_r[a], cfg.freq) for a in range(3)], axis=-1)
+    assert rel(V[0], V_ref) < 1e-6

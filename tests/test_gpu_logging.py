@@ -41,3 +41,12 @@ def test_window_station_matches_dense_lu(station, precond):
     H, _ = ie.ie_receiver_fields(ctx, e, np.array(rxw))
     Href = orx.receiver_H(n, (h, h, h), origin, k0, lg.SIGMA0, ds, X, rxw, txw, mw)
     assert rel(H[0], Href) < 1e-6
+
+
+def test_device_window_sigma_equals_the_host_recipe():
+    """The device (torch) sampling of the formation in the window frame equals the numpy recipe
+    (ie_workloads.logging.window_sigma) to roundoff on the window-1 shape at several stations."""
+    for tx in lg.stations(4):
+        a = lg.window_sigma(tx, (64, 32, 32), 0.25)
+        b = lg.window_sigma_device(tx, (64, 32, 32), 0.25).cpu().numpy()
+        assert np.abs(a - b).max() <= 1e-15 * np.abs(a).max()

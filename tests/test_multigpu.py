@@ -54,3 +54,72 @@ def test_bench_accounting_is_consistent():
         L = 2 * n[2]
         assert bench.kc_flops(*n) == 4 * n[0] * n[1] * (30 * L * math.log2(L) + 72 * L)
     assert abs(bench.FP64_NOMINAL_TFLOPS - 37.22496) < 1e-9
+
+
+def _sweep_worker(rank, ws, port, q):
+    import sys
+    import numpy as np
+    import torch.distributed as dist
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import bench
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=ws)
+    units = bench.sweep_units((0, 1, 2), (1e5, 4e5))
+    merged, mine = bench.distributed_sweep(units, _oracle_unit, rank, ws)
+    q.put((rank, mine, {k: v.tolist() for k, v in merged.items()}))
+    dist.destroy_process_group()
+
+
+def _oracle_unit(unit):
+    """One (frequency, station) system of a tiny layered sweep, solved by the oracle (dense LU of
+    the c4-recipe 8^3 mini with the physical table, E0 of the station's triaxial transmitter) ->
+    the 9 receiver couplings per source dipole by reciprocity."""
+    import numpy as np
+    from ie_workloads import make_config, layered_inputs as li, tool_frame
+    from oracle import layered as lay
+    f, s = unit
+    cfg = make_config("c4lmini")
+    med = li.medium(cfg, f)
+    F = tool_frame(70.0, 45.0)
+    tx = (0.05 + 0.1 * s) * F[2]
+    srcs = [(tx, F[i]) for i in range(3)]
+    rx = [tx + 0.6 * F[2]]
+    T = li.table(cfg, med)
+    sbz = lay.background_per_layer(cfg.n, cfg.origin, cfg.hvec, *cfg.background())
+    ds = lay.contrast_layered(cfg.sigma(), sbz)
+    E0 = li.incident(cfg, med, srcs)
+    e0rx, h0 = li.receiver_inputs(cfg, med, srcs, rx)
+    A = lay.dense_matrix_layered(T, ds)
+    out = []
+    for i in range(3):
+        E = np.linalg.solve(A, E0[i].ravel()).reshape(E0[i].shape)
+        out.append([lay.receiver_coupling(E, ds, e0rx[d], h0[i, d], cfg.h ** 3, med.omega) for d in range(len(e0rx))])
+    return np.array(out)
+
+
+@pytest.mark.timeout(300)
+def test_distributed_sweep_solves_each_unit_once_and_merges_like_one_rank():
+    """World size 2 (gloo): the (frequency, station) systems of a sweep are split between the
+    ranks, every unit is solved exactly once, and the merged receiver couplings equal the
+    single-rank run."""
+    import sys
+    import numpy as np
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import bench
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_sweep_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    out = sorted(q.get(timeout=250) for _ in ps)
+    for p in ps:
+        p.join(timeout=30)
+    units = bench.sweep_units((0, 1, 2), (1e5, 4e5))
+    mine = [tuple(u) for o in out for u in o[1]]
+    assert sorted(mine) == sorted(units) and len(mine) == len(set(mine))  # each unit exactly once
+    assert out[0][2].keys() == out[1][2].keys() == set(units)
+    single, _ = bench.distributed_sweep(units, _oracle_unit, 0, 1)
+    for u in units:
+        assert np.array_equal(np.array(out[0][2][u]), single[u])
+        assert np.array_equal(np.array(out[1][2][u]), single[u])
