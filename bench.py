@@ -49,6 +49,14 @@ def kernel_bytes(nx, ny, nz):
             "K-E x-inverse+update": 96 * N + 48 * N + 48 * N}
 
 
+def fused_kernel_bytes(nx, ny, nz):
+    """Compulsory HBM bytes per launch of the fused pairs (1 RHS): the X1 hand-off stays in L2.
+    K-AB reads x and dsigma, writes X2; K-DE reads X2 and x, writes y."""
+    N = nx * ny * nz
+    return {"K-AB contrast+x-forward+y-forward (fused)": 48 * N + 48 * N + 192 * N,
+            "K-DE y-inverse+x-inverse+update (fused)": 192 * N + 48 * N + 48 * N}
+
+
 FP64_NOMINAL_TFLOPS = 64 * 2 * 148 * 1.965e9 / 1e12  # 64 DFMA/clk/SM x 148 SMs at 1965 MHz = 37.2
 
 
@@ -334,7 +342,7 @@ def layered_leg(steps=10, name="c3"):
     flops = 8 * R * R * 4 * nx * ny * nrhs
     return {"workload": f"{name} (64^3, layers 1/0.01/1 S/m at -4/+4 m, physical table), {nrhs} RHS",
             "ms_per_apply": round(ms, 4),
-            "kernels_ms": {k: round(v[0] / max(1, v[1]), 4) for k, v in prof.items()},
+            "kernels_ms": {k: round(v[0] / max(1, v[1]), 4) for k, v in prof.items() if v[1] > 0},
             "k_c_prime": {"ms": round(kc_ms, 4), "alg_bytes": table + x2, "gbs": round((table + x2) / kc_ms / 1e6, 1),
                           "fp64_tflops": round(flops / kc_ms / 1e9, 2), "pipe": "DMMA m8n8k4 f64 (tensor cores)"},
             "host_generation_s": {"table": round(t_table, 2), "incident": round(t_e0, 2)},
@@ -405,22 +413,33 @@ def layered_dd_leg(name="c3capped", runs=(("full", 0), ("gauss_seidel", 0), ("ja
     return out
 
 
-def c4_layered_units(units, runs=(("full", 1), ("gauss_seidel", 1)), verbose=False, name="c4", outer_tol=None):
+C4_VARIANTS = (("c4", 1e-6, (("full", 1),)),
+               ("c4", 1e-3, (("full", 1), ("gauss_seidel", 1))),
+               ("c4mid", 1e-6, (("full", 1), ("gauss_seidel", 1), ("jacobi", 1))))
+
+
+def _run_key(name, tol, scheme, pc):
+    return f"{name}@{tol:g}:" + DD_KEYS[scheme] + ("_cie" if pc else "")
+
+
+def c4_layered_units(units, variants=C4_VARIANTS, verbose=False):
     """Solve (frequency, station) units of the c4 deviated-well sweep (BASELINE.json configs[3])
-    on the three-layer background.  Per frequency one context: the physical table is generated on
-    the host and uploaded once, the layered spectra are amortised over the stations (excluded from
-    s/position).  Per unit the host generates the layered E0 of the triaxial
-    transmitter and of the 9 receiver dipoles (1/3/7 m x tool axes) -- overlapped with the
-    previous unit's GPU work and reported apart -- and the GPU runs H2D + solve + receiver
-    couplings (device-timed).  Returns ({unit: {run: [s, iters, status]}}, info)."""
+    on the three-layer background, for every (config variant, outer tol, schemes) in `variants`
+    (variants share the background, hence the table: one context per frequency, the contrast is
+    swapped per variant).  The physical table is generated on the host and uploaded once per
+    frequency, its spectra amortised over the stations (excluded from s/position).
+    Per unit the host generates the layered E0 of the triaxial transmitter and of the 9 receiver
+    dipoles (1/3/7 m x tool axes) -- overlapped with the previous unit's GPU work and reported
+    apart -- and the GPU runs H2D + solve + receiver couplings (device-timed).
+    Returns ({unit: {run key: [s, gmres iters, status]}}, info)."""
     import concurrent.futures as cf
     import torch
     import paper_2306_17537_b200 as ie
     from ie_workloads import make_config, layered_inputs as li
     from ie_workloads.configs import c4_stations
-    cfg = make_config(name)
-    tol = cfg.outer_tol if outer_tol is None else outer_tol
-    sigma = torch.from_numpy(cfg.sigma()).cuda()
+    cfgs = {name: make_config(name) for name, _, _ in variants}
+    cfg = cfgs[variants[0][0]]
+    sig = {name: torch.from_numpy(c.sigma()).cuda() for name, c in cfgs.items()}
     st_all = c4_stations()
     info = {"table_s": {}, "setup_s": {}, "gen_s": []}
     res = {}
@@ -433,14 +452,18 @@ def c4_layered_units(units, runs=(("full", 1), ("gauss_seidel", 1)), verbose=Fal
         e0rx, h0 = li.receiver_inputs(cfg, med, srcs, st_all[s]["rx"])
         return E0, torch.from_numpy(e0rx).pin_memory(), h0, time.perf_counter() - t0
 
-    for f in sorted({u[0] for u in units}, key=lambda v: [u[0] for u in units].index(v)):
+    freqs = []
+    for u in units:
+        if u[0] not in freqs:
+            freqs.append(u[0])
+    for f in freqs:
         mine = [u for u in units if u[0] == f]
         t0 = time.perf_counter()
         med = li.medium(cfg, f)
         T = li.table(cfg, med)
         info["table_s"][str(f)] = round(time.perf_counter() - t0, 2)
         t0 = time.perf_counter()
-        ctx = _layered_ctx(cfg, T, sigma, 3, cfg.boxes, cfg.restart, freq=f)
+        ctx = _layered_ctx(cfg, T, sig[variants[0][0]], 3, cfg.boxes, cfg.restart, freq=f)
         torch.cuda.synchronize()
         info["setup_s"][str(f)] = round(time.perf_counter() - t0, 3)
         del T
@@ -451,50 +474,56 @@ def c4_layered_units(units, runs=(("full", 1), ("gauss_seidel", 1)), verbose=Fal
             if i + 1 < len(mine):
                 fut = pool.submit(gen, med, mine[i + 1][1])
             res[u] = {}
-            for scheme, pc in runs:
-                t, st, H = _layered_position(ctx, E0, e0rx, h0, scheme, cfg.boxes, tol, cfg.restart, pc)
-                k = DD_KEYS[scheme] + ("_cie" if pc else "")
-                res[u][k] = [t, st["total_inner_iters"], ie.STATUS.get(st["status"], st["status"])]
-                if verbose:
-                    print(f, u[1], k, round(t, 4), st["total_inner_iters"], st["sweeps"], st["e_final"], flush=True)
+            for name, tol, runs in variants:
+                ie.ie_set_contrast(ctx, sig[name])
+                for scheme, pc in runs:
+                    t, st, H = _layered_position(ctx, E0, e0rx, h0, scheme, cfg.boxes, tol, cfg.restart, pc)
+                    k = _run_key(name, tol, scheme, pc)
+                    res[u][k] = [t, st["total_inner_iters"], ie.STATUS.get(st["status"], st["status"])]
+                    if verbose:
+                        print(f, u[1], k, round(t, 4), st["total_inner_iters"], st["sweeps"], st["e_final"], flush=True)
         del ctx
         torch.cuda.empty_cache()
     pool.shutdown()
     return res, info
 
 
-def c4_layered_sweep(stations=(0, 31, 63), freqs=(4e5,), runs=(("full", 1), ("gauss_seidel", 1)), verbose=False,
-                     rank=0, ws=1, name="c4", outer_tol=None):
-    """The c4 sweep summary: s/position per scheme (sum over frequencies of one station's device
-    time, mean over stations).  With ws > 1 ranks the (frequency, station) units are split
-    between the ranks (replicas, no data-path collective) and the aggregate s/position is the
-    slowest rank's total device time over the number of stations."""
+def c4_layered_sweep(stations=(0, 31, 63), freqs=(4e5,), variants=C4_VARIANTS, verbose=False, rank=0, ws=1):
+    """The c4 sweep summary: s/position per (variant, tol, scheme) = the sum over frequencies of
+    one station's device time, mean over stations (reported only when every unit converged; the
+    measured time and statuses always).  With ws > 1 ranks the (frequency, station) units are
+    split between the ranks (replicas, no data-path collective) and the aggregate s/position is
+    the slowest rank's total device time over the number of stations."""
     units = sweep_units(stations, freqs)
     mine = rank_units(units, rank, ws)
     t0 = time.perf_counter()
-    res, info = c4_layered_units(mine, runs, verbose, name, outer_tol) if mine else ({}, {"table_s": {}, "setup_s": {}, "gen_s": []})
+    res, info = c4_layered_units(mine, variants, verbose) if mine else ({}, {"table_s": {}, "setup_s": {}, "gen_s": []})
     wall = time.perf_counter() - t0
     merged = gather_results(res, ws)
     infos = gather_results({rank: info}, ws)
-    out = {"workload": f"{name} sweep (128x128x64, layers 1/0.01/1 S/m, triaxial, rx 1/3/7 m x 3 axes)",
-           "outer_tol": outer_tol,
+    gens = [g for v in infos.values() for g in v["gen_s"]]
+    out = {"workload": "c4 sweep (128x128x64, layers 1/0.01/1 S/m at -4/+4 m, physical table; triaxial; "
+                       "rx 1/3/7 m x 3 tool axes by reciprocity); c4mid = the slab confined to the middle layer",
            "stations": list(stations), "freqs": list(freqs), "n_ranks": ws, "units": len(units),
            "table_s": {r: v["table_s"] for r, v in infos.items()}, "setup_s": {r: v["setup_s"] for r, v in infos.items()},
-           "generation_s_per_unit": round(float(np.mean([g for v in infos.values() for g in v["gen_s"]])), 2),
+           "generation_s_per_unit": round(float(np.mean(gens)), 2) if gens else None,
+           "generation": "host (layered_green): E0 of the 3 transmitter dipoles + 9 receiver dipoles per unit, "
+                         "overlapped with the previous unit's GPU work; excluded from s/position",
            "rank_wall_s": round(wall, 2)}
-    for scheme, pc in runs:
-        k = DD_KEYS[scheme] + ("_cie" if pc else "")
-        by_station = {}
-        for (f, s), r in merged.items():
-            by_station[s] = by_station.get(s, 0.0) + r[k][0]
-        rank_time = {}
-        for r in range(ws):
-            rank_time[r] = sum(merged[u][k][0] for u in rank_units(units, r, ws))
-        out[k] = {"s_per_position": round(float(np.mean(list(by_station.values()))), 4),
-                  "per_station_s": {str(s): round(t, 4) for s, t in sorted(by_station.items())},
-                  "gmres_iters": [merged[u][k][1] for u in units], "status": sorted({merged[u][k][2] for u in units})}
-        if ws > 1:
-            out[k]["aggregate_s_per_position"] = round(max(rank_time.values()) / len(stations), 4)
+    for name, tol, runs in variants:
+        for scheme, pc in runs:
+            k = _run_key(name, tol, scheme, pc)
+            by_station = {}
+            for (f, s), r in merged.items():
+                by_station[s] = by_station.get(s, 0.0) + r[k][0]
+            status = sorted({merged[u][k][2] for u in units})
+            mean = round(float(np.mean(list(by_station.values()))), 4)
+            out[k] = {"s_per_position": mean if status == ["IE_OK"] else None, "s_measured": mean,
+                      "per_station_s": {str(s): round(t, 4) for s, t in sorted(by_station.items())},
+                      "gmres_iters": [merged[u][k][1] for u in units], "status": status}
+            if ws > 1:
+                rank_time = {r: sum(merged[u][k][0] for u in rank_units(units, r, ws)) for r in range(ws)}
+                out[k]["aggregate_s_per_position"] = round(max(rank_time.values()) / len(stations), 4)
     return out
 
 
@@ -701,7 +730,7 @@ def run_ours(args, cfg, sigma, rank, ws, local):
     peak, peak_src = peaks()
 
     # roofline of the dominant kernel (largest share of the step)
-    kb = kernel_bytes(nx, ny, nz)
+    kb = dict(kernel_bytes(nx, ny, nz), **fused_kernel_bytes(nx, ny, nz))
     shares = {k: v[0] / max(1, v[1]) for k, v in prof.items() if v[1] > 0 and v[0] > 0}
     dom = max(shares, key=shares.get)
     achieved = kb[dom] / (shares[dom] / 1e3) / 1e9

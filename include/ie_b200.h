@@ -248,12 +248,16 @@ typedef struct {
 } ie_info;
 ie_status ie_get_info(const ie_ctx* ctx, ie_info* info);
 /* Per-kernel device timing of the operator (benchmarks).  enable != 0 starts recording CUDA
- * events around each of the five operator kernels (K-A x-forward+contrast, K-B y-forward,
- * K-C z-convolution, K-D y-inverse, K-E x-inverse+update) on the context stream; enable = 0
- * stops and clears.  ie_profile_read synchronises the stream and returns, for each kernel k,
- * the summed device time ms[k] (milliseconds) and the number of launches counts[k]. */
+ * events around each operator pass on the context stream: k = 0 K-A x-forward+contrast,
+ * 1 K-B y-forward, 2 K-C z-convolution, 3 K-D y-inverse, 4 K-E x-inverse+update, 5 K-DE (K-D
+ * and K-E fused in one persistent launch), 6 K-AB (K-A and K-B fused in one persistent launch);
+ * the fused pairs are opt-in (environment IE_FUSED_DE=1 / IE_FUSED_AB=1 when the context is
+ * created; measured slower than the separate passes); enable = 0 stops and clears.  ie_profile_read synchronises the
+ * stream and returns, for each slot k, the summed device time ms[k] (milliseconds) and the
+ * number of operator applications counts[k] that ran that pass (0 for passes replaced by a
+ * fused kernel).  Caller-owned host arrays of 7 entries. */
 ie_status ie_profile(ie_ctx* ctx, int32_t enable);
-ie_status ie_profile_read(ie_ctx* ctx, double* ms /*[5]*/, int32_t* counts /*[5]*/);
+ie_status ie_profile_read(ie_ctx* ctx, double* ms /*[7]*/, int32_t* counts /*[7]*/);
 /* Copy the packed Green spectrum of the given box shape (box = NULL: the grid) to the host:
  * complex128 [6][bz+1][by+1][bx+1], components (xx, yy, zz, xy, xz, yz), scaled by
  * 1/(8 bx by bz); entry (kx,ky,kz) of the full padded spectrum F[G_pq] (Eq. 10) is

@@ -31,7 +31,8 @@ EXPORTED = ("ie_create", "ie_destroy", "ie_last_error", "ie_workspace_query", "i
             "ie_profile", "ie_profile_read", "ie_receiver_fields_table", "ie_get_layer_spectrum")
 IE_TABLE_NONE, IE_TABLE_QUADRANT, IE_TABLE_HOMOGENEOUS = 0, 1, 2
 KERNELS = ("K-A x-forward+contrast", "K-B y-forward", "K-C z-convolution", "K-D y-inverse",
-           "K-E x-inverse+update")
+           "K-E x-inverse+update", "K-DE y-inverse+x-inverse+update (fused)",
+           "K-AB contrast+x-forward+y-forward (fused)")
 
 
 class IEError(RuntimeError):
@@ -334,8 +335,8 @@ def ie_profile(ctx, enable=True):
 
 def ie_profile_read(ctx):
     """Returns {kernel name: (total ms, launches)} for the operator kernels since ie_profile(ctx, True)."""
-    ms = np.zeros(5, np.float64)
-    cnt = np.zeros(5, np.int32)
+    ms = np.zeros(len(KERNELS), np.float64)
+    cnt = np.zeros(len(KERNELS), np.int32)
     _check(ctx, _lib.ie_profile_read(ctx.handle, _ptr(ms), _ptr(cnt)), "ie_profile_read")
     return {k: (float(ms[i]), int(cnt[i])) for i, k in enumerate(KERNELS)}
 

@@ -190,6 +190,8 @@ ie_status ie_create(const ie_grid* g, const ie_background* bg, double freq_hz, v
   c->omega = 2 * kPi * freq_hz;
   c->stream = (cudaStream_t)stream;
   if (const char* sl = getenv("IE_SLABS")) c->slabs = sl[0] == '1';  // opt-in slab pipeline
+  if (const char* fd = getenv("IE_FUSED_DE")) c->fused_de = fd[0] == '1';  // K-DE fused (opt-in)
+  if (const char* fa = getenv("IE_FUSED_AB")) c->fused_ab = fa[0] == '1';  // K-AB fused (opt-in)
   // k0 = sqrt(i omega mu0 sigma0), Re, Im > 0 (Eq. 7)
   c->k0 = std::sqrt(cplx(0.0, c->omega * kMu0 * c->sigma_b));
   // self term K(0) = (1/sigma0)[(2/3)(1 - i k0 a) e^{i k0 a} - 1]  (reading R3)
@@ -233,6 +235,7 @@ ie_status ie_destroy(ie_ctx* c) {
   cudaFree(c->e0);
   cudaFree(c->tw.dev);
   cudaFree(c->d_red);
+  cudaFree(c->fused_cnt);
   if (c->h_red) cudaFreeHost(c->h_red);
   for (auto ev : c->ev_pool) cudaEventDestroy(ev);
   if (c->aux_ready) {
@@ -869,7 +872,7 @@ ie_status ie_profile(ie_ctx* c, int32_t enable) {
 ie_status ie_profile_read(ie_ctx* c, double* ms, int32_t* counts) {
   if (!c || !ms || !counts) return fail(c, IE_ERR_INVALID_ARGUMENT, "profile_read: bad arguments");
   IE_CUDA(c, cudaStreamSynchronize(c->stream));
-  for (int k = 0; k < 5; ++k) {
+  for (int k = 0; k < kProfSlots; ++k) {
     ms[k] = 0;
     counts[k] = 0;
   }
@@ -880,9 +883,12 @@ ie_status ie_profile_read(ie_ctx* c, double* ms, int32_t* counts) {
     float t = 0;
     IE_CUDA(c, cudaEventElapsedTime(&t, c->ev_pool[mk.ev0], c->ev_pool[mk.ev1]));
     ms[mk.kernel] += t;
-    if (mk.kernel == 0) ++applies;
+    if (mk.kernel == 0 || mk.kernel == kProfFusedAB) ++applies;  // one front pass per application
   }
-  for (int k = 0; k < 5; ++k) counts[k] = applies;
+  // passes that ran: a fused kernel replaces its parts (those report 0 ms, 0 applications)
+  std::vector<int> ran(kProfSlots, 0);
+  for (auto& mk : c->ev_marks) ran[mk.kernel] = 1;
+  for (int k = 0; k < kProfSlots; ++k) counts[k] = ran[k] ? applies : 0;
   return IE_OK;
 }
 

@@ -19,6 +19,8 @@ constexpr double kPi = 3.14159265358979323846264338327950288;
 constexpr double kMu0 = 4e-7 * kPi;  // DESIGN.md reading R1
 constexpr int kMaxItems = 48;        // batch items per operator launch (kernel-parameter budget)
 constexpr int kMaxLog2 = 10;         // FFT lengths 2 .. 1024
+constexpr int kProfSlots = 7;        // ie_profile_read: K-A .. K-E, K-DE (fused), K-AB (fused)
+constexpr int kProfFusedDE = 5, kProfFusedAB = 6;
 
 // -------------------------------------------------------------------- operator batch
 // One operator application on one right-hand side / sub-domain.  The operator's domain is
@@ -119,6 +121,11 @@ struct ie_ctx {
   std::vector<Mark> ev_marks;
   size_t ev_used = 0;
   // L2-resident slab pipeline of the y/z passes (operator.cu): three streams, ring events
+  int* fused_cnt = nullptr;  // task / slot counters of the persistent fused operator kernels
+  // K-D + K-E / K-A + K-B as one persistent kernel each (X1 through an L2 ring): opt-in with
+  // IE_FUSED_DE=1 / IE_FUSED_AB=1 at create -- parity-tested, measured slower
+  bool fused_de = false;
+  bool fused_ab = false;
   bool slabs = false;
   bool aux_ready = false;
   cudaStream_t aux[3] = {};

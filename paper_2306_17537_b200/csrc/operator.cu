@@ -714,6 +714,314 @@ __global__ void __launch_bounds__(128) k_xinv(const __grid_constant__ ApplyParam
     }
 }
 
+// =====================================================================  K-DE (fused)
+// K-D and K-E in ONE persistent launch, the X1 hand-off through a small ring of plane buffers
+// that stays in L2 (so the 96N-byte X1 intermediate is neither written to nor read from HBM).
+// Work = planes P = (item, component, z); per plane NYT "Y-tasks" (the inverse y-FFT of 8
+// consecutive kx columns: X2 -> ring slot, rows y < ny) and NXT "X-tasks" (the inverse x-FFT
+// of RX rows of the slot -> crop -> identity update into y, exactly k_xinv's epilogue).  Tasks
+// are handed out in a fixed order by an atomic counter: group g = the Y-tasks of plane g, then
+// the X-tasks of plane g - D (lag D), so an X-task waits only on Y-tasks handed out earlier
+// (per-slot counter ydone), and a Y-task reusing a slot waits only on the X-tasks of the plane
+// S planes back (xdone), handed out earlier too (S > D): every wait is on strictly earlier
+// tasks, already held by running CTAs -> no deadlock for any residency.  Producer: stores
+// (plain stores: L1 is write-through), barrier, __threadfence + atomicAdd by one thread (cumulative); consumer: ld.acquire spin by one thread,
+// barrier, __threadfence, loads with ld.cg (the ring is rewritten within the launch, so no
+// L1 / non-coherent path).
+struct FusedSched {
+  int* cnt;  // [0] task counter, [1, 1+S) ydone, [1+S, 1+2S) xdone (zeroed before the launch)
+  int S, D, NP, NYT, NXT, RX;
+  long long slot_elems;  // ny * 2nx
+};
+
+__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void spin_until(const int* p, int target) {
+  int ns = 32;
+  while (ld_acquire_gpu(p) < target) {
+    __nanosleep(ns);
+    if (ns < 1024) ns *= 2;
+  }
+}
+
+template <int LY>
+struct FusedShape {
+  static constexpr int W = 8;                            // kx columns per Y-task
+  static constexpr int NT = W * FftPlan<LY>::T;          // threads per CTA
+};
+
+template <int LY, int LX, bool PRE>
+__global__ void __launch_bounds__(FusedShape<LY>::NT, 1024 / FusedShape<LY>::NT) k_yxinv(const __grid_constant__ ApplyParams p,
+                                                             const FusedSched fs) {
+  using PY = FftPlan<LY>;
+  using PX = FftPlan<LX>;
+  constexpr int W = FusedShape<LY>::W, NT = FusedShape<LY>::NT;
+  constexpr int TY = PY::T, VY = PY::V, R0Y = PY::radix(0, false), RLY = PY::radix(PY::NST - 1, false);
+  constexpr int TX = PX::T, VX = PX::V, R0X = PX::radix(0, false), RLX = PX::radix(PX::NST - 1, false);
+  static_assert(NT % TX == 0, "whole x-lines per CTA");
+  extern __shared__ double2 sm[];
+  const int nx = p.nx, ny = p.ny, nz = p.nz, Lx = 2 * nx;
+  const long long N = (long long)nx * ny * nz;
+  const int G = fs.NYT + fs.NXT;
+  const int D = fs.D, NP = fs.NP;
+  const long long total = (long long)NP * G;
+  int* ydone = fs.cnt + 1;
+  int* xdone = fs.cnt + 1 + fs.S;
+  __shared__ int s_next[2];
+  if (threadIdx.x == 0) s_next[0] = atomicAdd(fs.cnt, 1);
+  for (int iter = 0;; ++iter) {
+    __syncthreads();  // s_next[iter & 1] written; the previous task's smem use is over
+    const int task = s_next[iter & 1];
+    if (task >= total) break;
+    // the next task index is fetched now, its atomic latency hidden behind this task
+    if (threadIdx.x == 0) s_next[(iter + 1) & 1] = atomicAdd(fs.cnt, 1);
+    // decode the task order: D groups of Y only, NP - D groups of Y + X, D groups of X only
+    bool isy;
+    int plane, sub;
+    const int a = D * fs.NYT, b = a + (NP - D) * G;
+    if (task < a) {
+      isy = true;
+      plane = task / fs.NYT;
+      sub = task % fs.NYT;
+    } else if (task < b) {
+      const int r = task - a, g = r / G, w = r % G;
+      isy = w < fs.NYT;
+      plane = isy ? D + g : g;
+      sub = isy ? w : w - fs.NYT;
+    } else {
+      const int r = task - b;
+      isy = false;
+      plane = NP - D + r / fs.NXT;
+      sub = r % fs.NXT;
+    }
+    const int slot = plane % fs.S, gen = plane / fs.S;
+    double2* ring = p.X1 + (long long)slot * fs.slot_elems;
+    const int item = plane / (3 * nz), q = (plane / nz) % 3, z = plane % nz;
+    if (isy) {
+      const int c = threadIdx.x % W, t = threadIdx.x / W;
+      const int kx = sub * W + c;
+      const double2* src = p.X2 + (((long long)item * 3 + q) * nz + z) * (long long)LY * Lx + kx;
+      double2 v[1][VY];
+#pragma unroll
+      for (int u = 0; u < VY / R0Y; ++u)
+#pragma unroll
+        for (int r = 0; r < R0Y; ++r) v[0][u * R0Y + r] = src[(long long)(t + u * TY + r * (LY / R0Y)) * Lx];
+      auto idx = [&](int) { return SIdx{0, W, c}; };
+      fft_run<LY, false, +1, 1, false, true>(v, sm, idx, t, p.tw_y, false);
+      // the slot is free once the X-tasks of the plane S back have read it
+      if (gen > 0 && threadIdx.x == 0) spin_until(xdone + slot, fs.NXT * gen);
+      __syncthreads();
+      double2* dst = ring + kx;
+#pragma unroll
+      for (int u = 0; u < VY / RLY; ++u)
+#pragma unroll
+        for (int r = 0; r < RLY / 2; ++r) dst[(long long)(t + u * TY + r * (LY / RLY)) * Lx] = v[0][u * RLY + r];
+      __syncthreads();  // every store of the CTA issued; thread 0's fence is cumulative
+      if (threadIdx.x == 0) {
+        __threadfence();
+        atomicAdd(ydone + slot, 1);
+      }
+    } else {
+      if (threadIdx.x == 0) spin_until(ydone + slot, fs.NYT * (gen + 1));
+      __syncthreads();
+      const ApplyItem& it = p.items[item];
+      const int l = q;
+      const int lr = threadIdx.x / TX, t = threadIdx.x % TX;
+      const int yy = sub * fs.RX + lr;
+      const bool valid = yy < ny;
+      double2 v[1][VX];
+      {
+        const double2* src = ring + (long long)(valid ? yy : 0) * Lx;
+#pragma unroll
+        for (int u = 0; u < VX / R0X; ++u)
+#pragma unroll
+          for (int r = 0; r < R0X; ++r) v[0][u * R0X + r] = valid ? __ldcg(src + t + u * TX + r * (LX / R0X)) : czero();
+      }
+      const int region = padded(LX);
+      auto idx = [&](int) { return SIdx{lr * region, 1, 0}; };
+      fft_run<LX, false, +1, 1, false, true>(v, sm, idx, t, p.tw_x, false);
+      if (valid) {
+        const int zz = z;
+        const long long off = ((long long)zz * ny + yy) * nx;
+        const double al = p.alpha * it.xscale, be = p.beta;
+        double2* yrow = it.y + l * N + off;
+        const double2* xrow = it.x + l * N + off;
+        const int pc0 = l == 0 ? 0 : (l == 1 ? 3 : 4), pc1 = l == 0 ? 3 : (l == 1 ? 1 : 5),
+                  pc2 = l == 0 ? 4 : (l == 1 ? 5 : 2);
+        const double* prow = PRE ? it.pm + zz * p.ds_zs + yy * p.ds_ys : nullptr;
+        const double2* x0row = it.x + off;
+#pragma unroll
+        for (int u = 0; u < VX / RLX; ++u)
+#pragma unroll
+          for (int r = 0; r < RLX / 2; ++r) {  // x >= nx discarded (crop)
+            const int x = t + u * TX + r * (LX / RLX);
+            double2 o = cscale(v[0][u * RLX + r], be);
+            if (al != 0.0) {
+              double2 xi;
+              if constexpr (PRE) {
+                const double q0 = __ldg(prow + pc0 * p.ds_cs + x), q1 = __ldg(prow + pc1 * p.ds_cs + x),
+                             q2 = __ldg(prow + pc2 * p.ds_cs + x);
+                const double2 e0 = ld2(x0row + x), e1 = ld2(x0row + N + x), e2 = ld2(x0row + 2 * N + x);
+                xi = make_double2(q0 * e0.x + q1 * e1.x + q2 * e2.x, q0 * e0.y + q1 * e1.y + q2 * e2.y);
+              } else {
+                xi = ld2(xrow + x);
+              }
+              o.x = fma(al, xi.x, o.x);
+              o.y = fma(al, xi.y, o.y);
+            }
+            if (p.accumulate) o = cadd(o, yrow[x]);
+            yrow[x] = o;
+          }
+      }
+      __syncthreads();  // every ring read of this task has returned
+      if (threadIdx.x == 0) atomicAdd(xdone + slot, 1);
+    }
+  }
+}
+
+// =====================================================================  K-AB (fused)
+// K-A and K-B in one persistent launch, the same scheme as K-DE: planes P = (item, z) of the
+// source z-range; per plane NAT "A-tasks" (contrast J = dsigma x and the x-forward FFT of RA
+// rows, all three components: exactly k_xfwd, into a ring slot [3][ny][2nx]) and NBT =
+// 3 * 2nx/8 "B-tasks" (the y-forward FFT of 8 kx columns of one component: exactly k_yfwd,
+// ring -> X2).  Order: A-tasks of plane g, then B-tasks of plane g - D.
+template <int LX, int LY>
+__global__ void __launch_bounds__(FusedShape<LY>::NT, 512 / FusedShape<LY>::NT) k_xyfwd(const __grid_constant__ ApplyParams p,
+                                                                const FusedSched fs) {
+  using PX = FftPlan<LX>;
+  using PY = FftPlan<LY>;
+  constexpr int W = FusedShape<LY>::W, NT = FusedShape<LY>::NT;
+  constexpr int TX = PX::T, VX = PX::V, R0X = PX::radix(0, false), RLX = PX::radix(PX::NST - 1, false);
+  constexpr int TY = PY::T, VY = PY::V, R0Y = PY::radix(0, false), RLY = PY::radix(PY::NST - 1, false);
+  static_assert(NT % TX == 0, "whole x-lines per CTA");
+  extern __shared__ double2 sm[];
+  const int ny = p.ny, Lx = 2 * p.nx;
+  const int G = fs.NYT + fs.NXT;  // NYT: A-tasks per plane, NXT: B-tasks per plane
+  const int D = fs.D, NP = fs.NP;
+  const long long total = (long long)NP * G;
+  int* adone = fs.cnt + 1;
+  int* bdone = fs.cnt + 1 + fs.S;
+  const ApplyItem& it0 = p.items[0];
+  const int sbz = it0.sz1 - it0.sz0;
+  __shared__ int s_next[2];
+  if (threadIdx.x == 0) s_next[0] = atomicAdd(fs.cnt, 1);
+  for (int iter = 0;; ++iter) {
+    __syncthreads();
+    const int task = s_next[iter & 1];
+    if (task >= total) break;
+    if (threadIdx.x == 0) s_next[(iter + 1) & 1] = atomicAdd(fs.cnt, 1);
+    bool isa;
+    int plane, sub;
+    const int a = D * fs.NYT, b = a + (NP - D) * G;
+    if (task < a) {
+      isa = true;
+      plane = task / fs.NYT;
+      sub = task % fs.NYT;
+    } else if (task < b) {
+      const int r = task - a, g = r / G, w = r % G;
+      isa = w < fs.NYT;
+      plane = isa ? D + g : g;
+      sub = isa ? w : w - fs.NYT;
+    } else {
+      const int r = task - b;
+      isa = false;
+      plane = NP - D + r / fs.NXT;
+      sub = r % fs.NXT;
+    }
+    const int slot = plane % fs.S, gen = plane / fs.S;
+    double2* ring = p.X1 + (long long)slot * fs.slot_elems;  // [3][ny][2nx]
+    const int item = plane / sbz, zz = it0.sz0 + plane % sbz;
+    const ApplyItem& it = p.items[item];
+    if (isa) {
+      const int lr = threadIdx.x / TX, t = threadIdx.x % TX;
+      const int sbx = it.sx1 - it.sx0, sby = it.sy1 - it.sy0;
+      const int rowi = sub * fs.RX + lr;
+      const bool valid = rowi < sby;
+      const int yy = it.sy0 + (valid ? rowi : 0);
+      const long long sN = (long long)sbx * sby * sbz;
+      const double2* xrow = it.x + ((long long)(zz - it.sz0) * sby + (yy - it.sy0)) * sbx - it.sx0;
+      const double* srow = it.dsig + zz * p.ds_zs + yy * p.ds_ys;
+      const double xs = it.xscale;
+      double2 J[3][VX / 2];
+#pragma unroll
+      for (int u = 0; u < VX / R0X; ++u)
+#pragma unroll
+        for (int r = 0; r < R0X / 2; ++r) {
+          const int x = t + u * TX + r * (LX / R0X);
+          double2 J0 = czero(), J1 = czero(), J2 = czero();
+          if (valid && x >= it.sx0 && x < it.sx1) {
+            const double2 e0 = cscale(ld2(xrow + x), xs);
+            const double2 e1 = cscale(ld2(xrow + sN + x), xs);
+            const double2 e2 = cscale(ld2(xrow + 2 * sN + x), xs);
+            const double sxx = __ldg(srow + x), syy = __ldg(srow + p.ds_cs + x), szz = __ldg(srow + 2 * p.ds_cs + x);
+            const double sxy = __ldg(srow + 3 * p.ds_cs + x), sxz = __ldg(srow + 4 * p.ds_cs + x),
+                         syz = __ldg(srow + 5 * p.ds_cs + x);
+            J0 = make_double2(sxx * e0.x + sxy * e1.x + sxz * e2.x, sxx * e0.y + sxy * e1.y + sxz * e2.y);
+            J1 = make_double2(sxy * e0.x + syy * e1.x + syz * e2.x, sxy * e0.y + syy * e1.y + syz * e2.y);
+            J2 = make_double2(sxz * e0.x + syz * e1.x + szz * e2.x, sxz * e0.y + syz * e1.y + szz * e2.y);
+          }
+          J[0][u * (R0X / 2) + r] = J0;
+          J[1][u * (R0X / 2) + r] = J1;
+          J[2][u * (R0X / 2) + r] = J2;
+        }
+      const int region = padded(LX);
+      auto idx = [&](int) { return SIdx{lr * region, 1, 0}; };
+#pragma unroll
+      for (int l = 0; l < 3; ++l) {
+        double2 v[1][VX];
+#pragma unroll
+        for (int u = 0; u < VX / R0X; ++u)
+#pragma unroll
+          for (int r = 0; r < R0X; ++r) v[0][u * R0X + r] = r < R0X / 2 ? J[l][u * (R0X / 2) + r] : czero();
+        fft_run<LX, false, -1, 1, true>(v, sm, idx, t, p.tw_x, l > 0);
+        if (l == 0) {  // the slot is free once the B-tasks of the plane S back have read it
+          if (gen > 0 && threadIdx.x == 0) spin_until(bdone + slot, fs.NXT * gen);
+          __syncthreads();
+        }
+        if (valid) {
+          double2* out = ring + ((long long)l * ny + yy) * LX;
+#pragma unroll
+          for (int u = 0; u < VX / RLX; ++u)
+#pragma unroll
+            for (int r = 0; r < RLX; ++r) out[t + u * TX + r * (LX / RLX)] = v[0][u * RLX + r];
+        }
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        __threadfence();
+        atomicAdd(adone + slot, 1);
+      }
+    } else {
+      if (threadIdx.x == 0) spin_until(adone + slot, fs.NYT * (gen + 1));
+      __syncthreads();
+      const int nkx = Lx / W;
+      const int q = sub / nkx, kx = (sub % nkx) * W + threadIdx.x % W;
+      const int c = threadIdx.x % W, t = threadIdx.x / W;
+      const double2* src = ring + (long long)q * ny * Lx + kx;
+      double2 v[1][VY];
+#pragma unroll
+      for (int u = 0; u < VY / R0Y; ++u)
+#pragma unroll
+        for (int r = 0; r < R0Y; ++r) {
+          const int y = t + u * TY + r * (LY / R0Y);
+          v[0][u * R0Y + r] = (r < R0Y / 2 && y >= it.sy0 && y < it.sy1) ? __ldcg(src + (long long)y * Lx) : czero();
+        }
+      auto idx = [&](int) { return SIdx{0, W, c}; };
+      fft_run<LY, false, -1, 1, true>(v, sm, idx, t, p.tw_y, false);
+      double2* dst = p.X2 + (((long long)item * 3 + q) * p.nz + zz) * (long long)LY * Lx + kx;
+#pragma unroll
+      for (int u = 0; u < VY / RLY; ++u)
+#pragma unroll
+        for (int r = 0; r < RLY; ++r) dst[(long long)(t + u * TY + r * (LY / RLY)) * Lx] = v[0][u * RLY + r];
+      __syncthreads();  // every ring read of this task has returned
+      if (threadIdx.x == 0) atomicAdd(bdone + slot, 1);
+    }
+  }
+}
+
 // =====================================================================  host side
 // twiddle tables for every L = 2^p and both radix orders
 template <int L>
@@ -933,6 +1241,117 @@ static cudaError_t go_xinv(const ApplyParams& p, cudaStream_t s) {
   return p.items[0].pm ? go_xinv_p<L, true>(p, s) : go_xinv_p<L, false>(p, s);
 }
 
+// K-DE: persistent fused y-inverse + x-inverse (see the kernel); returns cudaErrorNotSupported
+// when the shape has no instance (the caller then runs K-D and K-E)
+// Lag D (planes) between a plane's producer and consumer tasks: more than the planes' worth
+// of tasks the resident CTAs hold at once, so a consumer rarely finds its plane unfinished;
+// ring slots S = D + 3 (a producer reusing a slot waits on the consumers S planes back).
+constexpr int kFusedMaxSlots = 120;  // counters: [1 + 2 S] ints per fused kernel, 256 reserved each
+static void fused_lag(int grid, int tasks_per_plane, int np, int* D, int* S) {
+  const int d = (grid + tasks_per_plane - 1) / tasks_per_plane + 2;
+  *S = std::max(1, std::min(std::min(np, d + 3), kFusedMaxSlots));
+  *D = std::max(0, std::min(d, *S - 1));
+}
+template <int LY, int LX, bool PRE>
+static cudaError_t go_yxinv_p(ie_ctx* c, const ApplyParams& p, cudaStream_t s) {
+  constexpr int NT = FusedShape<LY>::NT;
+  constexpr int TX = FftPlan<LX>::T, RX = NT / TX;
+  const size_t smem = (size_t)std::max(padded(LY * FusedShape<LY>::W), RX * padded(LX)) * sizeof(double2);
+  const void* kern = (const void*)k_yxinv<LY, LX, PRE>;
+  cudaError_t e = prep(kern, smem);
+  if (e) return e;
+  static int grid = 0;  // resident CTAs (per instance; the device is fixed for the process)
+  if (!grid) {
+    int dev = 0, sms = 0, per = 0;
+    if ((e = cudaGetDevice(&dev)) || (e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) ||
+        (e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, NT, smem)))
+      return e;
+    grid = std::max(1, per) * sms;
+  }
+  if (!c->fused_cnt && (e = cudaMalloc(&c->fused_cnt, 512 * sizeof(int)))) return e;
+  FusedSched fs;
+  fs.cnt = c->fused_cnt;
+  fs.NP = p.n_items * 3 * p.nz;
+  fs.NYT = 2 * p.nx / FusedShape<LY>::W;
+  fs.RX = RX;
+  fs.NXT = (p.ny + RX - 1) / RX;
+  fused_lag(grid, fs.NYT + fs.NXT, fs.NP, &fs.D, &fs.S);
+  fs.slot_elems = (long long)p.ny * 2 * p.nx;
+  if ((e = cudaMemsetAsync(c->fused_cnt, 0, (1 + 2 * fs.S) * sizeof(int), s))) return e;
+  const long long total = (long long)fs.NP * (fs.NYT + fs.NXT);
+  k_yxinv<LY, LX, PRE><<<(int)std::min<long long>(grid, total), NT, smem, s>>>(p, fs);
+  return cudaGetLastError();
+}
+template <int LY, int LX>
+static cudaError_t go_yxinv_l(ie_ctx* c, const ApplyParams& p, cudaStream_t s) {
+  return p.items[0].pm ? go_yxinv_p<LY, LX, true>(c, p, s) : go_yxinv_p<LY, LX, false>(c, p, s);
+}
+static cudaError_t go_yxinv(ie_ctx* c, const ApplyParams& p, cudaStream_t s) {
+  if (!c->fused_de || p.x2w != 2 * p.nx || p.k0x != 0) return cudaErrorNotSupported;
+  const int LY = 2 * p.ny, LX = 2 * p.nx;
+#define IE_FUSED_CASE(a, b) \
+  if (LY == a && LX == b) return go_yxinv_l<a, b>(c, p, s);
+  IE_FUSED_CASE(512, 512)
+  IE_FUSED_CASE(256, 512)
+  IE_FUSED_CASE(256, 256)
+  IE_FUSED_CASE(128, 256)
+  IE_FUSED_CASE(128, 128)
+  IE_FUSED_CASE(64, 128)
+  IE_FUSED_CASE(128, 64)
+  IE_FUSED_CASE(64, 64)
+#undef IE_FUSED_CASE
+  return cudaErrorNotSupported;
+}
+
+// K-AB: persistent fused contrast + x-forward + y-forward (see the kernel)
+template <int LX, int LY>
+static cudaError_t go_xyfwd_l(ie_ctx* c, const ApplyParams& p, cudaStream_t s) {
+  constexpr int NT = FusedShape<LY>::NT;
+  constexpr int TX = FftPlan<LX>::T, RA = NT / TX;
+  const size_t smem = (size_t)std::max(padded(LY * FusedShape<LY>::W), RA * padded(LX)) * sizeof(double2);
+  const void* kern = (const void*)k_xyfwd<LX, LY>;
+  cudaError_t e = prep(kern, smem);
+  if (e) return e;
+  static int grid = 0;
+  if (!grid) {
+    int dev = 0, sms = 0, per = 0;
+    if ((e = cudaGetDevice(&dev)) || (e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) ||
+        (e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, NT, smem)))
+      return e;
+    grid = std::max(1, per) * sms;
+  }
+  if (!c->fused_cnt && (e = cudaMalloc(&c->fused_cnt, 512 * sizeof(int)))) return e;
+  const ApplyItem& it = p.items[0];
+  FusedSched fs;
+  fs.cnt = c->fused_cnt + 256;  // its own counters (K-DE uses [0, 256))
+  fs.NP = p.n_items * (it.sz1 - it.sz0);
+  fs.RX = RA;
+  fs.NYT = (it.sy1 - it.sy0 + RA - 1) / RA;  // A-tasks per plane
+  fs.NXT = 3 * (2 * p.nx / FusedShape<LY>::W);  // B-tasks per plane
+  fused_lag(grid, fs.NYT + fs.NXT, std::min(fs.NP, p.nz * p.n_items), &fs.D, &fs.S);  // ring <= X1
+  fs.slot_elems = 3LL * p.ny * 2 * p.nx;
+  if ((e = cudaMemsetAsync(fs.cnt, 0, (1 + 2 * fs.S) * sizeof(int), s))) return e;
+  const long long total = (long long)fs.NP * (fs.NYT + fs.NXT);
+  k_xyfwd<LX, LY><<<(int)std::min<long long>(grid, total), NT, smem, s>>>(p, fs);
+  return cudaGetLastError();
+}
+static cudaError_t go_xyfwd(ie_ctx* c, const ApplyParams& p, cudaStream_t s) {
+  if (!c->fused_ab || p.x2w != 2 * p.nx || p.k0x != 0) return cudaErrorNotSupported;
+  const int LY = 2 * p.ny, LX = 2 * p.nx;
+#define IE_FUSED_CASE(a, b) \
+  if (LX == a && LY == b) return go_xyfwd_l<a, b>(c, p, s);
+  IE_FUSED_CASE(512, 512)
+  IE_FUSED_CASE(512, 256)
+  IE_FUSED_CASE(256, 256)
+  IE_FUSED_CASE(256, 128)
+  IE_FUSED_CASE(128, 128)
+  IE_FUSED_CASE(128, 64)
+  IE_FUSED_CASE(64, 128)
+  IE_FUSED_CASE(64, 64)
+#undef IE_FUSED_CASE
+  return cudaErrorNotSupported;
+}
+
 template <int L> static void wrap_xfwd(cudaError_t* e, const ApplyParams& p, cudaStream_t s, int m) { *e = go_xfwd<L>(p, s, m); }
 template <int L> static void wrap_yfwd(cudaError_t* e, const ApplyParams& p, cudaStream_t s, int m) { *e = go_yfwd<L>(p, s, m); }
 template <int L> static void wrap_zconv(cudaError_t* e, const ApplyParams& p, cudaStream_t s) { *e = go_zconv<L>(p, s); }
@@ -984,12 +1403,22 @@ static cudaError_t run_apply(ie_ctx* c, const ApplyParams& p, cudaStream_t s) {
   if ((e = pr.take(6, &ev))) return e;
   // items of one launch share the source y/z range (K-A rows, K-B planes)
   pr.rec(ev + 0, s);
-  IE_DISPATCH_L(2 * p.nx, wrap_xfwd, &e, p, s, max_rows);
-  if (e) return e;
-  pr.rec(ev + 1, s);
-  IE_DISPATCH_L(2 * p.ny, wrap_yfwd, &e, p, s, max_planes);
-  if (e) return e;
-  pr.rec(ev + 2, s);
+  bool ab = false;
+  e = go_xyfwd(c, p, s);  // K-AB fused (X1 through an L2-resident ring) where instantiated
+  if (e == cudaSuccess) {
+    ab = true;
+    pr.rec(ev + 2, s);
+  } else {
+    if (e != cudaErrorNotSupported) return e;
+    (void)cudaGetLastError();
+    e = cudaSuccess;
+    IE_DISPATCH_L(2 * p.nx, wrap_xfwd, &e, p, s, max_rows);
+    if (e) return e;
+    pr.rec(ev + 1, s);
+    IE_DISPATCH_L(2 * p.ny, wrap_yfwd, &e, p, s, max_planes);
+    if (e) return e;
+    pr.rec(ev + 2, s);
+  }
   if (p.mhat) {  // layered background: z-z' contraction per horizontal wavenumber (layered.cu)
     e = launch_zlayer(p, s);
   } else if (const int W16 = zconv16_width(2 * p.nz, 2 * p.nx)) {
@@ -999,13 +1428,37 @@ static cudaError_t run_apply(ie_ctx* c, const ApplyParams& p, cudaStream_t s) {
   }
   if (e) return e;
   pr.rec(ev + 3, s);
+  // forward marks: K-A, K-B separately or K-AB fused; K-C
+  auto mark_front = [&]() {
+    if (ab) {
+      pr.mark(kProfFusedAB, ev + 0, ev + 2);
+    } else {
+      pr.mark(0, ev + 0, ev + 1);
+      pr.mark(1, ev + 1, ev + 2);
+    }
+    pr.mark(2, ev + 2, ev + 3);
+  };
+  const int nfront = ab ? 2 : 3;
+  e = go_yxinv(c, p, s);  // K-DE fused (X1 through an L2-resident ring) where instantiated
+  if (e == cudaSuccess) {
+    pr.rec(ev + 4, s);
+    mark_front();
+    pr.mark(kProfFusedDE, ev + 3, ev + 4);
+    c->launches += nfront + 1;
+    return e;
+  }
+  if (e != cudaErrorNotSupported) return e;
+  (void)cudaGetLastError();
+  e = cudaSuccess;
   IE_DISPATCH_L(2 * p.ny, wrap_yinv, &e, p, s);
   if (e) return e;
   pr.rec(ev + 4, s);
   IE_DISPATCH_L(2 * p.nx, wrap_xinv, &e, p, s);
   pr.rec(ev + 5, s);
-  for (int k = 0; k < 5; ++k) pr.mark(k, ev + k, ev + k + 1);
-  c->launches += 5;
+  mark_front();
+  pr.mark(3, ev + 3, ev + 4);
+  pr.mark(4, ev + 4, ev + 5);
+  c->launches += nfront + 2;
   return e;
 }
 

@@ -121,3 +121,44 @@ def test_fullsize_multi_rhs_equals_single_rhs(name):
         y1 = torch.empty_like(x[r:r + 1])
         ie.ie_apply_operator(ctx, x[r:r + 1].contiguous(), y1)
         assert torch.equal(y1[0], y3[r]), r
+
+
+@pytest.mark.parametrize("name,boxes", [("c5", False), ("c4h", False), ("c4h", True), ("c2mod", True)])
+@pytest.mark.parametrize("precond", [0, 1])
+def test_fused_passes_match_the_five_pass_schedule_bitwise(name, boxes, precond):
+    """K-AB (K-A + K-B) and K-DE (K-D + K-E), each one persistent launch handing X1 through an
+    L2-resident ring of plane buffers with per-slot producer/consumer counters, run the same
+    per-element arithmetic as the separate passes: identical operator output for every on/off
+    combination (IE_FUSED_AB / IE_FUSED_DE = 1 at context creation select the fused passes),
+    on the grid and on every DD box (z-restricted sources included), with and without the
+    contraction IE."""
+    import os
+    import torch
+    import paper_2306_17537_b200 as ie
+    cfg = make_config(name)
+    sigma = cfg.sigma()
+    outs = []
+    for ab, de in (("1", "1"), ("0", "1"), ("1", "0"), ("0", "0")):
+        os.environ["IE_FUSED_AB"], os.environ["IE_FUSED_DE"] = ab, de
+        try:
+            ctx, _ = gpu_ctx(cfg, sigma=sigma, boxes=cfg.boxes if boxes else [], nrhs=1, restart=2)
+        finally:
+            os.environ.pop("IE_FUSED_AB", None)
+            os.environ.pop("IE_FUSED_DE", None)
+        res = []
+        for b in (cfg.boxes if boxes else [None]):
+            bn = (b[1] - b[0], b[3] - b[2], b[5] - b[4]) if b else cfg.n
+            x = torch.randn((1, 3, bn[2], bn[1], bn[0]), dtype=torch.complex128, device="cuda",
+                            generator=torch.Generator(device="cuda").manual_seed(5))
+            y = torch.empty_like(x)
+            if precond:
+                ie.ie_solve_subdomain(ctx, x, y.copy_(x), tol=1e-3, restart=2, max_iters=2, box=b, check=False,
+                                      precond=1)
+            else:
+                ie.ie_apply_operator(ctx, x, y, box=b)
+            torch.cuda.synchronize()
+            res.append(y.cpu())
+        outs.append(res)
+    for other in outs[1:]:
+        for a, b in zip(outs[0], other):
+            assert torch.equal(a, b)

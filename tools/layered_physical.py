@@ -13,7 +13,7 @@ ap.add_argument("--what", default="op,c3capped,c3,c4")
 ap.add_argument("--stations", default="0,31,63")
 ap.add_argument("--freqs", default="4e5")
 ap.add_argument("--c4runs", default="full:1,gauss_seidel:1")
-ap.add_argument("--c4name", default="c4")
+ap.add_argument("--c4name", default="default")
 ap.add_argument("--tol", type=float, default=None)
 a = ap.parse_args()
 w = a.what.split(",")
@@ -28,8 +28,10 @@ if "c3" in w:
     out["dd_c3"] = bench.layered_dd_leg("c3", runs=(("full", 1), ("gauss_seidel", 1), ("full", 0)), reps=0)
     print(json.dumps(out["dd_c3"]), flush=True)
 if "c4" in w:
-    runs = tuple((r.split(":")[0], int(r.split(":")[1])) for r in a.c4runs.split(","))
+    variants = bench.C4_VARIANTS
+    if a.c4name != "default":
+        runs = tuple((r.split(":")[0], int(r.split(":")[1])) for r in a.c4runs.split(","))
+        variants = ((a.c4name, a.tol if a.tol else 1e-6, runs),)
     out["c4"] = bench.c4_layered_sweep(tuple(int(x) for x in a.stations.split(",")),
-                                       tuple(float(x) for x in a.freqs.split(",")), runs, verbose=True,
-                                       name=a.c4name, outer_tol=a.tol)
+                                       tuple(float(x) for x in a.freqs.split(",")), variants, verbose=True)
     print(json.dumps(out["c4"]), flush=True)

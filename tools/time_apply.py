@@ -35,5 +35,5 @@ e1.record()
 t1 = time.perf_counter()
 torch.cuda.synchronize()
 t2 = time.perf_counter()
-print(f"{a.config} slabs={os.environ.get('IE_NO_SLABS', '0') != '1'} ms/apply {e0.elapsed_time(e1) / a.steps:.4f} "
+print(f"{a.config} ms/apply {e0.elapsed_time(e1) / a.steps:.4f} "
       f"host-enqueue ms/apply {(t1 - t0) * 1e3 / a.steps:.4f} wall ms/apply {(t2 - t0) * 1e3 / a.steps:.4f}")
