@@ -336,6 +336,12 @@ def make_config(name):
                       sources=[(np.zeros(3), zdip)],
                       receivers=[np.array([0.0, 0.0, 1.0]), np.array([0.0, 0.0, 3.0])],
                       boxes=box_grid((256, 256, 128), (4, 4, 1)), restart=50, outer_tol=1e-6)
+    if name == "c5jac":
+        return Config(name, (128, 128, 128), 0.2, 0.5, 1e5, 5, _c5_sigma,
+                      sources=[(np.zeros(3), zdip)], receivers=[np.array([0.0, 0.0, 1.0])],
+                      boxes=box_grid((128, 128, 128), (2, 2, 1)), restart=50, outer_tol=1e-6,
+                      note="the c5 recipe on 128^3 with 2x2 boxes of 64x64x128 (the c5 box shape): the "
+                           "oracle's block Jacobi runs here sweep by sweep beside the GPU's")
     if name == "c5mini":
         return Config(name, (8, 8, 8), 0.2, 0.5, 1e5, 5, lambda rng, c: _c5_sigma(rng, c, corr_len=0.4, block=2),
                       sources=[(np.zeros(3), zdip)], receivers=[np.array([0.0, 0.0, 1.0])],
@@ -344,4 +350,4 @@ def make_config(name):
 
 
 CONFIG_NAMES = ("c1", "c2", "c2capped", "c2mod", "c2mini", "c3h", "c3mini", "c4h", "c5", "c5mini",
-                "c3", "c3capped", "c3lmini", "c3lminicapped", "c4", "c4mid", "c4lmini")
+                "c3", "c3capped", "c3lmini", "c3lminicapped", "c4", "c4mid", "c4lmini", "c5jac")

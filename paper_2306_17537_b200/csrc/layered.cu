@@ -315,14 +315,23 @@ __global__ void __launch_bounds__(288, 2) k_zlayer_tma(const __grid_constant__ A
     }
   }
   __syncthreads();
+  // a chunk of KC source rows (q nz + k', one q: nz is a multiple of KC) matters only if its k'
+  // range meets the items' source range [z0, z1) (z-restricted Gauss-Seidel couplings); the
+  // producer and the consumers skip the same chunks
+  auto active = [&](int ch) {
+    const int kp0 = (ch * KC) % nz;
+    return kp0 + KC > z0 && kp0 < z1;
+  };
   if (warp == NCW) {  // ---- producer
     if (lane == 0) {
-      for (int ch = 0; ch < nchunks; ++ch) {
-        const int st = ch % NST;
-        if (ch >= NST) mbar_wait(&empty[st], ((ch / NST) - 1) & 1);
+      for (int ch = 0, a = 0; ch < nchunks; ++ch) {
+        if (!active(ch)) continue;
+        const int st = a % NST;
+        if (a >= NST) mbar_wait(&empty[st], ((a / NST) - 1) & 1);
         const uint32_t bytes = (uint32_t)(KC * R * sizeof(double2));
         mbar_arrive_expect_tx(&full[st], bytes);
         bulk_g2s(ring + st * KC * R, M + (long long)ch * KC * R, bytes, &full[st]);
+        ++a;
       }
     }
     return;
@@ -361,9 +370,11 @@ __global__ void __launch_bounds__(288, 2) k_zlayer_tma(const __grid_constant__ A
   for (int r = 0; r < RT; ++r)
 #pragma unroll
     for (int t = 0; t < NT; ++t) c1[r][t][0] = c1[r][t][1] = c2[r][t][0] = c2[r][t][1] = 0.0;
-  for (int ch = 0; ch < nchunks; ++ch) {
-    const int st = ch % NST;
-    mbar_wait(&full[st], (ch / NST) & 1);
+  for (int ch = 0, ach = 0; ch < nchunks; ++ch) {
+    if (!active(ch)) continue;
+    const int st = ach % NST;
+    mbar_wait(&full[st], (ach / NST) & 1);
+    ++ach;
     const double2* A = ring + st * KC * R;
     // all operands of the chunk's KC/4 k-steps loaded before the first DMMA (their shared-memory
     // latencies overlap)
