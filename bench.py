@@ -422,7 +422,27 @@ def _run_key(name, tol, scheme, pc):
     return f"{name}@{tol:g}:" + DD_KEYS[scheme] + ("_cie" if pc else "")
 
 
-def c4_layered_units(units, variants=C4_VARIANTS, verbose=False):
+def shared_table(cfg, med, rank=0, ws=1):
+    """The layered table of (cfg, frequency): generated on the host by rank 0 alone (all its
+    cores) and broadcast to the other ranks over the process group (NCCL over NVLink on GPUs;
+    input distribution, not a data-path collective) -- N ranks would otherwise each rebuild the
+    same 9.7 GB table with 1/N of the host cores."""
+    from ie_workloads import layered_inputs as li
+    if ws <= 1:
+        return li.table(cfg, med)
+    import torch
+    import torch.distributed as dist
+    from threadpoolctl import threadpool_limits
+    nx, ny, nz = cfg.n
+    buf = torch.empty((3, 3, nz, nz, ny, nx), dtype=torch.complex128, device="cuda")
+    if rank == 0:
+        with threadpool_limits(len(os.sched_getaffinity(0))):
+            buf.copy_(torch.from_numpy(li.table(cfg, med)))
+    dist.broadcast(buf, 0)
+    return buf.cpu().numpy()
+
+
+def c4_layered_units(units, variants=C4_VARIANTS, verbose=False, rank=0, ws=1, all_freqs=None):
     """Solve (frequency, station) units of the c4 deviated-well sweep (BASELINE.json configs[3])
     on the three-layer background, for every (config variant, outer tol, schemes) in `variants`
     (variants share the background, hence the table: one context per frequency, the contrast is
@@ -453,15 +473,17 @@ def c4_layered_units(units, variants=C4_VARIANTS, verbose=False):
         return E0, torch.from_numpy(e0rx).pin_memory(), h0, time.perf_counter() - t0
 
     freqs = []
-    for u in units:
+    for u in (units if all_freqs is None else [(f, None) for f in all_freqs]):
         if u[0] not in freqs:
             freqs.append(u[0])
     for f in freqs:
         mine = [u for u in units if u[0] == f]
         t0 = time.perf_counter()
         med = li.medium(cfg, f)
-        T = li.table(cfg, med)
+        T = shared_table(cfg, med, rank, ws)  # every rank takes part in each frequency's broadcast
         info["table_s"][str(f)] = round(time.perf_counter() - t0, 2)
+        if not mine:
+            continue
         t0 = time.perf_counter()
         ctx = _layered_ctx(cfg, T, sig[variants[0][0]], 3, cfg.boxes, cfg.restart, freq=f)
         torch.cuda.synchronize()
@@ -497,7 +519,7 @@ def c4_layered_sweep(stations=(0, 31, 63), freqs=(4e5,), variants=C4_VARIANTS, v
     units = sweep_units(stations, freqs)
     mine = rank_units(units, rank, ws)
     t0 = time.perf_counter()
-    res, info = c4_layered_units(mine, variants, verbose) if mine else ({}, {"table_s": {}, "setup_s": {}, "gen_s": []})
+    res, info = c4_layered_units(mine, variants, verbose, rank, ws, all_freqs=freqs)
     wall = time.perf_counter() - t0
     merged = gather_results(res, ws)
     infos = gather_results({rank: info}, ws)
@@ -888,6 +910,8 @@ def main():
     assert ws == args.gpus, f"--gpus {args.gpus} but WORLD_SIZE {ws}"
     if ws > 1:  # the scaling run: operator replicas + the distributed c4 sweep only
         args.no_cufft = args.no_layered = args.no_dd = args.no_window = True
+        from threadpoolctl import threadpool_limits  # torchrun sets 1 thread per rank: share the host
+        threadpool_limits(max(1, len(os.sched_getaffinity(0)) // ws))
     cfg = make_config(args.config)
     sigma = cfg.sigma()
     if args.impl == "reference":
