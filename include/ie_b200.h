@@ -156,11 +156,15 @@ typedef struct {
   int32_t max_iters; /* cap on A v products */
   int32_t min_iters; /* >= 0 */
   double tol;        /* relative residual target, > 0 */
-  int32_t precond;   /* 0: the paper's conventional IE; 1: contraction-IE right preconditioner
-                        P = 2 sigma_b (sigma + sigma_b I)^-1 per cell (Hursan & Zhdanov; the paper's
-                        remedy for high contrast): GMRES on (I - G dsigma) P chi = E0,
-                        E = P chi -- same solution, same Eq. 9 residual */
 } ie_gmres_opts;
+
+/* Right preconditioner of every subsequent GMRES on this context (ie_solve_subdomain, the
+ * sub-domain and full-domain solves of ie_solve_dd): kind 0 = none, the paper's conventional IE
+ * (the default); kind 1 = the contraction-IE right preconditioner P = 2 sigma_b (sigma +
+ * sigma_b I)^-1 per cell (Hursan & Zhdanov; the paper's remedy for high contrast):
+ * GMRES on (I - G dsigma) P chi = E0, E = P chi -- same solution, same Eq. 9 residual (SURVEY
+ * 8(f)-2), built lazily from the contrast.  INVALID_ARGUMENT for other kinds. */
+ie_status ie_set_preconditioner(ie_ctx* ctx, int32_t kind);
 typedef struct {
   int32_t iters, restarts, converged;
   double relres_est, relres_true;
@@ -213,11 +217,13 @@ typedef struct {
   int32_t* iters;
 } ie_dd_stats;
 
-/* Solve for all n_src sources set by ie_set_source / ie_set_incident.
- * e_dev: [n_src][3][nz][ny][nx]; initial iterate on entry if init_from_e != 0, otherwise the
- * library starts from E0 (Algorithm 1 "initialize E^0 := E^(0)"); total field on exit.
- * Synchronous. */
-ie_status ie_solve_dd(ie_ctx* ctx, const ie_dd_opts* opts, void* e_dev, int32_t init_from_e, ie_dd_stats* stats);
+/* Solve for all n_src sources set by ie_set_source / ie_set_incident, starting from E0
+ * (Algorithm 1 "initialize E^0 := E^(0)").  e_dev: [n_src][3][nz][ny][nx], the total
+ * field on exit.  Synchronous. */
+ie_status ie_solve_dd(ie_ctx* ctx, const ie_dd_opts* opts, void* e_dev, ie_dd_stats* stats);
+/* The same with a caller-supplied initial iterate: e_dev holds it on entry (warm start, e.g. the
+ * previous tool position), the total field on exit. */
+ie_status ie_solve_dd_warm(ie_ctx* ctx, const ie_dd_opts* opts, void* e_dev, ie_dd_stats* stats);
 
 /* Magnetic field at receiver points for every source (Eq. 4):
  * H(r) = H0(r) + sum_c grad g(r - r_c) x (dsigma_c E_c) dv   (G^H of Eq. 6 applied to J),

@@ -27,7 +27,8 @@ SCHEMES = {"full": IE_DD_FULL, "jacobi": IE_DD_JACOBI, "gauss_seidel": IE_DD_GAU
 
 EXPORTED = ("ie_create", "ie_destroy", "ie_last_error", "ie_workspace_query", "ie_bind_workspace",
             "ie_set_contrast", "ie_set_source", "ie_get_incident", "ie_set_incident", "ie_apply_operator",
-            "ie_solve_subdomain", "ie_solve_dd", "ie_receiver_fields", "ie_get_info", "ie_get_green_octant",
+            "ie_solve_subdomain", "ie_solve_dd", "ie_solve_dd_warm", "ie_set_preconditioner", "ie_receiver_fields",
+            "ie_get_info", "ie_get_green_octant",
             "ie_profile", "ie_profile_read", "ie_receiver_fields_table", "ie_get_layer_spectrum")
 IE_TABLE_NONE, IE_TABLE_QUADRANT, IE_TABLE_HOMOGENEOUS = 0, 1, 2
 KERNELS = ("K-A x-forward+contrast", "K-B y-forward", "K-C z-convolution", "K-D y-inverse",
@@ -59,7 +60,7 @@ class ie_box(ctypes.Structure):
 
 class ie_gmres_opts(ctypes.Structure):
     _fields_ = [("restart", ctypes.c_int32), ("max_iters", ctypes.c_int32), ("min_iters", ctypes.c_int32),
-                ("tol", ctypes.c_double), ("precond", ctypes.c_int32)]
+                ("tol", ctypes.c_double)]
 
 
 class ie_solve_stats(ctypes.Structure):
@@ -108,7 +109,9 @@ def load_library(path=LIB_PATH):
         "ie_apply_operator": [P, ctypes.POINTER(ie_box), I, P, P],
         "ie_solve_subdomain": [P, ctypes.POINTER(ie_box), I, P, P, ctypes.POINTER(ie_gmres_opts),
                                ctypes.POINTER(ie_solve_stats)],
-        "ie_solve_dd": [P, ctypes.POINTER(ie_dd_opts), P, I, ctypes.POINTER(ie_dd_stats)],
+        "ie_solve_dd": [P, ctypes.POINTER(ie_dd_opts), P, ctypes.POINTER(ie_dd_stats)],
+        "ie_solve_dd_warm": [P, ctypes.POINTER(ie_dd_opts), P, ctypes.POINTER(ie_dd_stats)],
+        "ie_set_preconditioner": [P, I],
         "ie_receiver_fields": [P, P, I, P, P, P],
         "ie_get_info": [P, ctypes.POINTER(ie_info)],
         "ie_get_green_octant": [P, ctypes.POINTER(ie_box), P],
@@ -267,9 +270,15 @@ def ie_apply_operator(ctx, x, y, box=None):
     _check(ctx, _lib.ie_apply_operator(ctx.handle, _box(box), int(nrhs), _ptr(x), _ptr(y)), "ie_apply_operator")
 
 
+def ie_set_preconditioner(ctx, kind):
+    """0: conventional IE (the paper's); 1: contraction-IE right preconditioner, for every later solve."""
+    _check(ctx, _lib.ie_set_preconditioner(ctx.handle, int(kind)), "ie_set_preconditioner")
+
+
 def ie_solve_subdomain(ctx, b, x, tol, restart=30, max_iters=5000, min_iters=0, box=None, check=True, precond=0):
     nrhs = b.shape[0] if b.dim() == 5 else 1
-    o = ie_gmres_opts(int(restart), int(max_iters), int(min_iters), float(tol), int(precond))
+    ie_set_preconditioner(ctx, precond)
+    o = ie_gmres_opts(int(restart), int(max_iters), int(min_iters), float(tol))
     st = (ie_solve_stats * nrhs)()
     s = _lib.ie_solve_subdomain(ctx.handle, _box(box), int(nrhs), _ptr(b), _ptr(x), ctypes.byref(o), st)
     stats = [dict(iters=t.iters, restarts=t.restarts, converged=bool(t.converged), relres_est=t.relres_est,
@@ -288,12 +297,14 @@ def ie_solve_dd(ctx, e, scheme, boxes=(), outer_tol=1e-8, adaptive=True, inner_t
     arr = (ie_box * max(nb, 1))(*[ie_box(*[int(v) for v in b]) for b in boxes])
     o = ie_dd_opts(SCHEMES[scheme] if isinstance(scheme, str) else int(scheme), arr, nb, float(outer_tol),
                    int(bool(adaptive)), float(inner_tol_fixed), float(inner_tol_factor), int(max_sweeps),
-                   ie_gmres_opts(int(restart), int(max_iters), int(min_iters), 0.0, int(precond)))
+                   ie_gmres_opts(int(restart), int(max_iters), int(min_iters), 0.0))
+    ie_set_preconditioner(ctx, precond)
     e_hist = np.zeros(((max_sweeps + 1), ns), np.float64)
     iters = np.zeros((max(max_sweeps, 1), max(nb, 1), ns), np.int32)
     st = ie_dd_stats(0, 0, 0, 0, 0.0, e_hist.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
                      iters.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)))
-    s = _lib.ie_solve_dd(ctx.handle, ctypes.byref(o), _ptr(e), int(bool(init_from_e)), ctypes.byref(st))
+    fn = _lib.ie_solve_dd_warm if init_from_e else _lib.ie_solve_dd
+    s = fn(ctx.handle, ctypes.byref(o), _ptr(e), ctypes.byref(st))
     out = dict(sweeps=st.sweeps, total_inner_iters=st.total_inner_iters, full_applies=st.full_applies,
                sub_applies=st.sub_applies, e_final=st.e_final, e_hist=e_hist[:st.sweeps + 1].copy(),
                iters=iters[:st.sweeps].copy(), status=s)

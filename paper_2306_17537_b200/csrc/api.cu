@@ -52,7 +52,7 @@ static const double* at_box(const ie_ctx* c, const double* grid6, const ie_box& 
   return grid6 + ((long long)b.k0 * c->g.ny + b.j0) * c->g.nx + b.i0;
 }
 
-// a GMRES system on box b; with the contraction-IE right preconditioner (opts precond = 1)
+// a GMRES system on box b; with the contraction-IE right preconditioner (ie_set_preconditioner 1)
 // the operator is (I - G dsigma) P, P = 2 sigma_b (sigma + sigma_b I)^-1
 static GmresSystem make_sys(const ie_ctx* c, const double2* b_, double2* x_, const ie_box& b, double tol,
                             int min_iters, int precond) {
@@ -345,8 +345,7 @@ ie_status ie_solve_subdomain(ie_ctx* c, const ie_box* box, int32_t nrhs, const v
   if (!c || nrhs < 1 || !b_dev || !x_dev || !o || !stats || o->restart < 1 || o->restart > 128 || !(o->tol > 0))
     return fail(c, IE_ERR_INVALID_ARGUMENT, "solve_subdomain: bad arguments");
   if (!c->contrast_set) return fail(c, IE_ERR_STATE, "solve before set_contrast");
-  if (o->precond < 0 || o->precond > 1) return fail(c, IE_ERR_INVALID_ARGUMENT, "solve_subdomain: precond 0 or 1");
-  if (o->precond) {
+  if (c->precond_kind) {
     ie_status sp = ensure_precond(c);
     if (sp) return sp;
   }
@@ -358,7 +357,7 @@ ie_status ie_solve_subdomain(ie_ctx* c, const ie_box* box, int32_t nrhs, const v
   std::vector<GmresSystem> sys;
   for (int r = 0; r < nrhs; ++r)
     sys.push_back(make_sys(c, (const double2*)b_dev + r * nb, (double2*)x_dev + r * nb, b, o->tol, o->min_iters,
-                           o->precond));
+                           c->precond_kind));
   Arena ar = arena_of(c);
   std::vector<GmresResult> res;
   ie_status st = gmres_batched(c, ar, bx, by, bz, b.k0, (long long)c->g.nx * c->g.ny, c->g.nx, sys, o->restart,
@@ -381,13 +380,29 @@ ie_status ie_solve_subdomain(ie_ctx* c, const ie_box* box, int32_t nrhs, const v
 }
 
 // ------------------------------------------------------------------------ Algorithm 1
-ie_status ie_solve_dd(ie_ctx* c, const ie_dd_opts* o, void* e_dev, int32_t init_from_e, ie_dd_stats* stats) {
+ie_status ie_set_preconditioner(ie_ctx* c, int32_t kind) {
+  if (!c) return fail(c, IE_ERR_INVALID_ARGUMENT, "set_preconditioner: null context");
+  if (kind < 0 || kind > 1) return fail(c, IE_ERR_INVALID_ARGUMENT, "set_preconditioner: kind 0 or 1");
+  c->precond_kind = kind;
+  return IE_OK;
+}
+
+static ie_status solve_dd_impl(ie_ctx* c, const ie_dd_opts* o, void* e_dev, int32_t init_from_e, ie_dd_stats* stats);
+
+ie_status ie_solve_dd(ie_ctx* c, const ie_dd_opts* o, void* e_dev, ie_dd_stats* stats) {
+  return solve_dd_impl(c, o, e_dev, 0, stats);
+}
+
+ie_status ie_solve_dd_warm(ie_ctx* c, const ie_dd_opts* o, void* e_dev, ie_dd_stats* stats) {
+  return solve_dd_impl(c, o, e_dev, 1, stats);
+}
+
+static ie_status solve_dd_impl(ie_ctx* c, const ie_dd_opts* o, void* e_dev, int32_t init_from_e, ie_dd_stats* stats) {
   if (!c || !o || !e_dev || !stats) return fail(c, IE_ERR_INVALID_ARGUMENT, "solve_dd: bad arguments");
   if (!c->contrast_set || !c->e0 || c->n_src < 1) return fail(c, IE_ERR_STATE, "solve_dd needs contrast and sources");
-  if (o->inner.restart < 1 || o->inner.restart > 128 || !(o->outer_tol > 0) || o->max_sweeps < 0 ||
-      o->inner.precond < 0 || o->inner.precond > 1)
+  if (o->inner.restart < 1 || o->inner.restart > 128 || !(o->outer_tol > 0) || o->max_sweeps < 0)
     return fail(c, IE_ERR_INVALID_ARGUMENT, "solve_dd: bad options");
-  if (o->inner.precond) {
+  if (c->precond_kind) {
     ie_status sp = ensure_precond(c);
     if (sp) return sp;
   }
@@ -407,7 +422,7 @@ ie_status ie_solve_dd(ie_ctx* c, const ie_dd_opts* o, void* e_dev, int32_t init_
   if (o->scheme == IE_DD_FULL) {
     std::vector<GmresSystem> sys;
     for (int r = 0; r < ns; ++r)
-      sys.push_back(make_sys(c, c->e0 + r * len, E + r * len, fb, o->outer_tol, o->inner.min_iters, o->inner.precond));
+      sys.push_back(make_sys(c, c->e0 + r * len, E + r * len, fb, o->outer_tol, o->inner.min_iters, c->precond_kind));
     std::vector<GmresResult> res;
     long long ap = 0;
     ie_status st = gmres_batched(c, ar, c->g.nx, c->g.ny, c->g.nz, 0, (long long)c->g.nx * c->g.ny, c->g.nx, sys, m,
@@ -538,7 +553,7 @@ ie_status ie_solve_dd(ie_ctx* c, const ie_dd_opts* o, void* e_dev, int32_t init_
       for (int r : rr) {
         const double thr = o->adaptive ? e[r] * o->inner_tol_factor : o->inner_tol_fixed;
         sys.push_back(make_sys(c, Bb + boff[i] + r * nbox(i), Xb + boff[i] + r * nbox(i), o->boxes[i], thr,
-                               std::max(1, o->inner.min_iters), o->inner.precond));
+                               std::max(1, o->inner.min_iters), c->precond_kind));
         who.push_back({i, r});
       }
     std::vector<GmresResult> res;
@@ -590,7 +605,7 @@ ie_status ie_solve_dd(ie_ctx* c, const ie_dd_opts* o, void* e_dev, int32_t init_
           std::vector<GmresSystem> sys;
           for (int i : g.second)
             sys.push_back(make_sys(c, Bb + boff[i] + r * nbox(i), Xb + boff[i] + r * nbox(i), o->boxes[i], thr,
-                                   std::max(1, o->inner.min_iters), o->inner.precond));
+                                   std::max(1, o->inner.min_iters), c->precond_kind));
           const ie_box& b0 = o->boxes[g.second[0]];
           std::vector<GmresResult> res;
           const size_t mark = ar.used;
@@ -619,7 +634,7 @@ ie_status ie_solve_dd(ie_ctx* c, const ie_dd_opts* o, void* e_dev, int32_t init_
         launch_gather(c, Tr, bb, o->boxes[i], 1, 0, 0);
         launch_axpby(c, xb, 0.0, bb, 0.0, nullptr, nbox(i));
         std::vector<GmresSystem> sys{make_sys(c, bb, xb, o->boxes[i], thr, std::max(1, o->inner.min_iters),
-                                              o->inner.precond)};
+                                              c->precond_kind)};
         const ie_box& b0 = o->boxes[i];
         std::vector<GmresResult> res;
         const size_t mark = ar.used;

@@ -99,6 +99,7 @@ struct ie_ctx {
   int n_src = 0;
   std::vector<double> src_pos, src_mom;  // host copies of the dipoles (for H0 at receivers)
   bool contrast_set = false;
+  int precond_kind = 0;  // ie_set_preconditioner: 0 none, 1 contraction IE
   // contraction-IE right preconditioner, built on first use: sym6 [6][N] each
   double* pre_p = nullptr;   // P = 2 sigma_b (sigma + sigma_b I)^-1
   double* pre_a = nullptr;   // a = P^-1

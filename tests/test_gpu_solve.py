@@ -264,3 +264,30 @@ def test_tall_grid_dd_matches_oracle_gmres(n, boxes, scheme):
     st = ie.ie_solve_dd(ctx, e, scheme, boxes=cfg.boxes, outer_tol=1e-9, restart=30, max_sweeps=300)
     assert st["e_final"] <= 1e-9
     assert rel(e.cpu().numpy()[0], Xref) < FIELD_TOL
+
+
+@pytest.mark.parametrize("scheme", ["full", "gauss_seidel", "jacobi"])
+def test_warm_start_and_preconditioner_calls(scheme):
+    """ie_solve_dd_warm starts from the caller's iterate (a converged field: 0 sweeps / iterations,
+    the field unchanged up to the final residual check); ie_solve_dd starts from E0 whatever e_dev
+    holds; ie_set_preconditioner persists across solves and rejects unknown kinds."""
+    import torch
+    import paper_2306_17537_b200 as ie
+    cfg = make_config("c2mini")
+    ctx, sigma = gpu_ctx(cfg)
+    k0, ds, E0, X = _lu_truth(cfg, sigma)
+    e = _field(cfg, 1)
+    st = ie.ie_solve_dd(ctx, e, scheme, boxes=cfg.boxes, outer_tol=1e-10, restart=30, max_sweeps=300)
+    assert rel(e.cpu().numpy(), X) < FIELD_TOL
+    e_conv = e.clone()
+    st2 = ie.ie_solve_dd(ctx, e, scheme, boxes=cfg.boxes, outer_tol=1e-10, restart=30, init_from_e=True)
+    assert st2["total_inner_iters"] == 0 and st2["sweeps"] == 0
+    assert torch.equal(e, e_conv)
+    e.fill_(1e3)  # cold start ignores the content
+    st3 = ie.ie_solve_dd(ctx, e, scheme, boxes=cfg.boxes, outer_tol=1e-10, restart=30, max_sweeps=300)
+    assert st3["total_inner_iters"] == st["total_inner_iters"] and rel(e.cpu().numpy(), X) < FIELD_TOL
+    with pytest.raises(ie.IEError):
+        ie.ie_set_preconditioner(ctx, 2)
+    ie.ie_set_preconditioner(ctx, 1)
+    st4 = ie.ie_solve_dd(ctx, e, scheme, boxes=cfg.boxes, outer_tol=1e-10, restart=30, max_sweeps=300, precond=1)
+    assert rel(e.cpu().numpy(), X) < FIELD_TOL and st4["e_final"] <= 1e-10
