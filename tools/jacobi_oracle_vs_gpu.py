@@ -21,10 +21,18 @@ ap.add_argument("--config", default="c5jac")
 ap.add_argument("--sweeps", type=int, default=20)
 ap.add_argument("--out", default="gpurun_out/jacobi_oracle_vs_gpu.json")
 ap.add_argument("--no-oracle", action="store_true")
+ap.add_argument("--splits", default=None, help="box splits sx,sy,sz (default: the config's boxes)")
+ap.add_argument("--n", default=None, help="grid nx,ny,nz overriding the config's (same recipe)")
 a = ap.parse_args()
 cfg = make_config(a.config)
+if a.n:
+    cfg.n = tuple(int(v) for v in a.n.split(","))
+    out_n = cfg.n
+if a.splits:
+    from ie_workloads import box_grid
+    cfg.boxes = box_grid(cfg.n, tuple(int(v) for v in a.splits.split(",")))
 sigma = cfg.sigma()
-out = {"config": a.config, "grid": list(cfg.n), "boxes": cfg.boxes, "outer_tol": cfg.outer_tol, "runs": []}
+out = {"config": a.config, "grid": list(cfg.n), "boxes": [list(b) for b in cfg.boxes], "outer_tol": cfg.outer_tol, "runs": []}
 ctx = ie.ie_create(cfg.n, cfg.hvec, cfg.origin, cfg.sigma_b, cfg.freq)
 ie.ensure_workspace(ctx, boxes=cfg.boxes, nrhs=1, restart=cfg.restart)
 ie.ie_set_contrast(ctx, torch.from_numpy(sigma).cuda())
