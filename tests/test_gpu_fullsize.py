@@ -123,8 +123,8 @@ def test_fullsize_multi_rhs_equals_single_rhs(name):
         assert torch.equal(y1[0], y3[r]), r
 
 
-@pytest.mark.parametrize("name,boxes", [("c5", False), ("c4h", False), ("c4h", True), ("c2mod", True)])
-@pytest.mark.parametrize("precond", [0, 1])
+@pytest.mark.parametrize("name,boxes,precond", [("c5", False, 0), ("c4h", False, 1), ("c4h", True, 0),
+                                                 ("c2mod", True, 1)])
 def test_fused_passes_match_the_five_pass_schedule_bitwise(name, boxes, precond):
     """K-AB (K-A + K-B) and K-DE (K-D + K-E), each one persistent launch handing X1 through an
     L2-resident ring of plane buffers with per-slot producer/consumer counters, run the same

@@ -15,6 +15,7 @@ ap.add_argument("--freqs", default="4e5")
 ap.add_argument("--c4runs", default="full:1,gauss_seidel:1")
 ap.add_argument("--c4name", default="default")
 ap.add_argument("--tol", type=float, default=None)
+ap.add_argument("--out", default=None)
 a = ap.parse_args()
 w = a.what.split(",")
 out = {}
@@ -32,6 +33,9 @@ if "c4" in w:
     if a.c4name != "default":
         runs = tuple((r.split(":")[0], int(r.split(":")[1])) for r in a.c4runs.split(","))
         variants = ((a.c4name, a.tol if a.tol else 1e-6, runs),)
-    out["c4"] = bench.c4_layered_sweep(tuple(int(x) for x in a.stations.split(",")),
+    st = tuple(range(64)) if a.stations == "all" else tuple(int(x) for x in a.stations.split(","))
+    out["c4"] = bench.c4_layered_sweep(st,
                                        tuple(float(x) for x in a.freqs.split(",")), variants, verbose=True)
     print(json.dumps(out["c4"]), flush=True)
+if a.out:
+    json.dump(out, open(a.out, "w"))
