@@ -435,11 +435,17 @@ def shared_table(cfg, med, rank=0, ws=1):
     from threadpoolctl import threadpool_limits
     nx, ny, nz = cfg.n
     buf = torch.empty((3, 3, nz, nz, ny, nx), dtype=torch.complex128, device="cuda")
+    T = None
     if rank == 0:
         with threadpool_limits(len(os.sched_getaffinity(0))):
-            buf.copy_(torch.from_numpy(li.table(cfg, med)))
+            T = li.table(cfg, med)
+        buf.copy_(torch.from_numpy(T))
     dist.broadcast(buf, 0)
-    return buf.cpu().numpy()
+    if T is None:
+        T = buf.cpu().numpy()
+    del buf
+    torch.cuda.empty_cache()
+    return T
 
 
 def c4_layered_units(units, variants=C4_VARIANTS, verbose=False, rank=0, ws=1, all_freqs=None):
