@@ -107,6 +107,7 @@ static ie_status apply_many(ie_ctx* c, Arena& ar, const ie_box& dom, const ie_bo
       it.dsig = dsig_at(c, dom);
       it.pm = nullptr;
       it.xscale = 1.0;
+      it.xscale_dev = nullptr;
       it.sx0 = src.i0;
       it.sx1 = src.i1;
       it.sy0 = src.j0;
@@ -192,6 +193,7 @@ ie_status ie_create(const ie_grid* g, const ie_background* bg, double freq_hz, v
   if (const char* sl = getenv("IE_SLABS")) c->slabs = sl[0] == '1';  // opt-in slab pipeline
   if (const char* fd = getenv("IE_FUSED_DE")) c->fused_de = fd[0] == '1';  // K-DE fused (opt-in)
   if (const char* fa = getenv("IE_FUSED_AB")) c->fused_ab = fa[0] == '1';  // K-AB fused (opt-in)
+  if (const char* gd = getenv("IE_GMRES_DEVICE")) c->gmres_device = gd[0] == '1';  // device Arnoldi (opt-in)
   // k0 = sqrt(i omega mu0 sigma0), Re, Im > 0 (Eq. 7)
   c->k0 = std::sqrt(cplx(0.0, c->omega * kMu0 * c->sigma_b));
   // self term K(0) = (1/sigma0)[(2/3)(1 - i k0 a) e^{i k0 a} - 1]  (reading R3)
@@ -237,6 +239,8 @@ ie_status ie_destroy(ie_ctx* c) {
   cudaFree(c->d_red);
   cudaFree(c->fused_cnt);
   if (c->h_red) cudaFreeHost(c->h_red);
+  if (c->h_arnflag) cudaFreeHost(c->h_arnflag);
+  for (auto ev : c->ev_arn) cudaEventDestroy(ev);
   for (auto ev : c->ev_pool) cudaEventDestroy(ev);
   if (c->aux_ready) {
     for (auto st : c->aux) cudaStreamDestroy(st);

@@ -34,8 +34,15 @@ struct ApplyItem {
   const double* pm;    // contraction-IE right preconditioner P (sym6, same strides) or null:
                        // the identity term becomes P x (the operator applied is (I - G dsigma) P)
   double xscale;
+  const double* xscale_dev;  // if non-null: the scale is *xscale_dev (device-side GMRES basis scales)
   int sx0, sx1, sy0, sy1, sz0, sz1;
 };
+
+#ifdef __CUDACC__
+__device__ __forceinline__ double item_xscale(const ApplyItem& it) {
+  return it.xscale_dev ? *it.xscale_dev : it.xscale;
+}
+#endif
 
 struct ApplyParams {
   int nx, ny, nz;
@@ -112,6 +119,11 @@ struct ie_ctx {
   double2* h_red = nullptr;
   size_t h_red_cap = 0;
   double2* d_red = nullptr;  // device mirror for coefficient uploads
+  bool gmres_device = false;  // Arnoldi recurrences on the device (IE_GMRES_DEVICE=1 at create)
+  int* h_arnflag = nullptr;  // mapped pinned [m][S] step flags of the device-side Arnoldi
+  int* d_arnflag = nullptr;  // its device alias
+  size_t h_arn_cap = 0;
+  std::vector<cudaEvent_t> ev_arn;  // one per Arnoldi step of a cycle (look-ahead)
   size_t d_red_cap = 0;
   // per-kernel profiling of the operator (ie_profile): events[i] brackets kernel kind[i]
   bool profiling = false;

@@ -26,6 +26,7 @@ struct DotJob {
   const double2* V;  // first basis vector; vector j at V + j * len
   int nv;            // number of basis vectors (dots); row nv gets ||w||^2 in .x
   int row;           // output row base
+  const int* enable = nullptr;  // device flag: the job is skipped when *enable == 0 (null: always run)
 };
 struct AxpyJob {
   double2* out;
@@ -33,6 +34,7 @@ struct AxpyJob {
   const double2* V;
   int nv;
   int coef;  // offset into the coefficient array
+  const int* enable = nullptr;
 };
 
 __device__ __forceinline__ double2 shfl_down2(double2 v, int d) {
@@ -49,6 +51,7 @@ __global__ void __launch_bounds__(256) k_mdot(const DotJob* __restrict__ jobs, l
   const DotJob jb = jobs[blockIdx.z];
   const int g0 = blockIdx.y * G;
   if (g0 > jb.nv) return;
+  if (jb.enable && *jb.enable == 0) return;
   __shared__ double2 red[8][G];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   double2 acc[G];
@@ -116,6 +119,7 @@ __global__ void __launch_bounds__(256) k_maxpy(const AxpyJob* __restrict__ jobs,
                                                long long len) {
   constexpr int G = 8;
   const AxpyJob jb = jobs[blockIdx.y];
+  if (jb.enable && *jb.enable == 0) return;
   __shared__ double2 cf[160];
   for (int j = threadIdx.x; j < jb.nv; j += blockDim.x) cf[j] = coefs[jb.coef + j];
   __syncthreads();
@@ -132,6 +136,235 @@ __global__ void __launch_bounds__(256) k_maxpy(const AxpyJob* __restrict__ jobs,
       }
     }
     jb.out[i] = cadd(a0, a1);
+  }
+}
+
+// ------------------------------------------------------- device-side Arnoldi recurrences
+// The Hessenberg column, DGKS test, Givens rotations and stopping rule of one Arnoldi step run on
+// the device (one CTA / thread per system), so a GMRES cycle is enqueued without a host round trip
+// per step: the host reads each step's "still iterating" flags one step late (look-ahead 1; a
+// finished system's extra step is skipped by every kernel but the operator) and reads the
+// recurrences back at the end of the cycle.  Same formulas, same order as the host path.
+struct ArnState {
+  double2* H;     // [S][m][m+1] column-major per system: H[(s m + k)(m+1) + j]
+  double2* cs;    // [S][m]
+  double2* sn;    // [S][m]
+  double2* g;     // [S][m+1]
+  double* scale;  // [S][m+1] basis scales 1/beta
+  double2* h;     // [S][m+1] current column
+  double* beta2;  // [S]
+  double* bnorm;  // [S]
+  double* tol;    // [S]
+  double* est;    // [S]
+  int* flag;      // [S] 1 while the system iterates in the cycle
+  int* reorth;    // [S] DGKS second pass requested
+  int* kdone;     // [S] Arnoldi steps done in the cycle
+  int* iters;     // [S] total iterations
+  int* miniters;  // [S]
+  int* brk;       // [S] breakdown (non-finite)
+  int m, maxiters;
+};
+
+__device__ __forceinline__ double2 cconj(double2 a) { return make_double2(a.x, -a.y); }
+__device__ __forceinline__ double cabs2(double2 a) { return a.x * a.x + a.y * a.y; }
+
+// Per-step jobs of the live systems, passed by value (no per-step job upload): system s's basis
+// is V + s * sys_stride, w = V_{k+1}; its reduction rows and coefficients start at s * (m + 2).
+struct ArnJobs {
+  double2* V;
+  long long sys_stride, len;
+  int k, nlive;
+  const int* enable;  // per-system flag array (flag or reorth)
+  int ids[kMaxItems];
+};
+
+// multi-dot <V_j, w> (j <= k) and ||w||^2 of the live systems (k_mdot's body, jobs by value)
+template <int G>
+__global__ void __launch_bounds__(256) k_mdot_arn(const __grid_constant__ ArnJobs jb, double2* __restrict__ part,
+                                                  int nblk, int st2) {
+  const int s = jb.ids[blockIdx.z];
+  const int nv = jb.k + 1;
+  const int g0 = blockIdx.y * G;
+  if (g0 > nv || !jb.enable[s]) return;
+  const long long len = jb.len;
+  const double2* Vb = jb.V + s * jb.sys_stride;
+  const double2* w = Vb + (long long)(jb.k + 1) * len;
+  __shared__ double2 red[8][G];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  double2 acc[G];
+#pragma unroll
+  for (int g = 0; g < G; ++g) acc[g] = czero();
+  const long long stride = (long long)nblk * 256;
+  for (long long i = blockIdx.x * 256LL + threadIdx.x; i < len; i += 2 * stride) {
+    const long long i2 = i + stride;
+    const bool ok2 = i2 < len;
+    double2 wv[2], v[2][G];
+    wv[0] = w[i];
+    wv[1] = ok2 ? w[i2] : czero();
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const bool on = g0 + g < nv;
+      v[0][g] = on ? Vb[(long long)(g0 + g) * len + i] : czero();
+      v[1][g] = (on && ok2) ? Vb[(long long)(g0 + g) * len + i2] : czero();
+    }
+#pragma unroll
+    for (int e = 0; e < 2; ++e)
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        if (g0 + g < nv) {
+          acc[g].x = fma(v[e][g].x, wv[e].x, fma(v[e][g].y, wv[e].y, acc[g].x));
+          acc[g].y = fma(v[e][g].x, wv[e].y, fma(-v[e][g].y, wv[e].x, acc[g].y));
+        } else if (g0 + g == nv) {
+          acc[g].x = fma(wv[e].x, wv[e].x, fma(wv[e].y, wv[e].y, acc[g].x));
+        }
+      }
+  }
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) acc[g] = cadd(acc[g], shfl_down2(acc[g], d));
+  }
+  if (lane == 0)
+#pragma unroll
+    for (int g = 0; g < G; ++g) red[wid][g] = acc[g];
+  __syncthreads();
+  if (threadIdx.x < G) {
+    const int j = g0 + threadIdx.x;
+    double2 sum = czero();
+    for (int w8 = 0; w8 < 8; ++w8) sum = cadd(sum, red[w8][threadIdx.x]);
+    if (j <= nv) part[((long long)s * st2 + j) * nblk + blockIdx.x] = sum;
+  }
+}
+
+// V_{k+1} -= sum_j coef_j V_j for the live systems (k_maxpy's body, jobs by value)
+__global__ void __launch_bounds__(256) k_maxpy_arn(const __grid_constant__ ArnJobs jb,
+                                                   const double2* __restrict__ coefs, int st2) {
+  constexpr int G = 8;
+  const int s = jb.ids[blockIdx.y];
+  if (!jb.enable[s]) return;
+  const int nv = jb.k + 1;
+  const long long len = jb.len;
+  const double2* Vb = jb.V + s * jb.sys_stride;
+  double2* out = jb.V + s * jb.sys_stride + (long long)(jb.k + 1) * len;
+  __shared__ double2 cf[160];
+  for (int j = threadIdx.x; j < nv; j += blockDim.x) cf[j] = coefs[(long long)s * st2 + j];
+  __syncthreads();
+  for (long long i = blockIdx.x * 256LL + threadIdx.x; i < len; i += (long long)gridDim.x * 256) {
+    double2 a0 = out[i], a1 = czero();
+    for (int j0 = 0; j0 < nv; j0 += G) {
+      double2 v[G];
+#pragma unroll
+      for (int g = 0; g < G; ++g) v[g] = j0 + g < nv ? Vb[(long long)(j0 + g) * len + i] : czero();
+#pragma unroll
+      for (int g = 0; g < G; g += 2) {
+        if (j0 + g < nv) a0 = cadd(a0, cmul(cf[j0 + g], v[g]));
+        if (j0 + g + 1 < nv) a1 = cadd(a1, cmul(cf[j0 + g + 1], v[g + 1]));
+      }
+    }
+    out[i] = cadd(a0, a1);
+  }
+}
+
+// Reduce the step's rows (one warp per row, fixed order), then h_j = <V_j, w> scale_j, the
+// multi-axpy coefficients -h_j scale_j, beta^2 = ||w||^2 - sum |h_j|^2 and (pass 0) the DGKS
+// request; pass 1 (always launched) then runs the step's Givens update (thread 0), so a step
+// without re-orthogonalisation costs no extra launch beyond the two skipped pass-1 kernels.
+__device__ void arn_givens(ArnState& a, int s, int k) {
+  const int m = a.m;
+  a.iters[s] += 1;
+  // (reorth stays set for the pass-1 axpy launched after this kernel; the next step's pass 0
+  // rewrites it; a stopping system clears it: its V_{k+1} is never used)
+  if (a.brk[s]) {
+    a.flag[s] = 0;
+    a.reorth[s] = 0;
+    return;
+  }
+  const double beta = sqrt(fmax(a.beta2[s], 0.0));
+  double2* Hk = a.H + ((long long)s * m + k) * (m + 1);
+  double2* cs = a.cs + s * m;
+  double2* sn = a.sn + s * m;
+  double2* g = a.g + s * (m + 1);
+  for (int j = 0; j <= k; ++j) Hk[j] = a.h[s * (m + 1) + j];
+  Hk[k + 1] = make_double2(beta, 0.0);
+  for (int j = 0; j < k; ++j) {  // previous rotations
+    const double2 t = cadd(cmul(cs[j], Hk[j]), cmul(sn[j], Hk[j + 1]));
+    Hk[j + 1] = csub(cmul(cconj(cs[j]), Hk[j + 1]), cmul(cconj(sn[j]), Hk[j]));
+    Hk[j] = t;
+  }
+  const double2 aa = Hk[k], bb = Hk[k + 1];
+  const double den = sqrt(cabs2(aa) + cabs2(bb));
+  if (den == 0.0) {
+    cs[k] = make_double2(1.0, 0.0);
+    sn[k] = czero();
+  } else {
+    cs[k] = cconj(make_double2(aa.x / den, aa.y / den));
+    sn[k] = cconj(make_double2(bb.x / den, bb.y / den));
+  }
+  Hk[k] = cadd(cmul(cs[k], aa), cmul(sn[k], bb));
+  Hk[k + 1] = czero();
+  const double2 gk = g[k], ns = cconj(sn[k]);
+  g[k + 1] = make_double2(-(ns.x * gk.x - ns.y * gk.y), -(ns.x * gk.y + ns.y * gk.x));
+  g[k] = cmul(cs[k], gk);
+  a.kdone[s] = k + 1;
+  const double est = sqrt(cabs2(g[k + 1])) / a.bnorm[s];
+  a.est[s] = est;
+  const bool happy = !(beta > 1e-14 * sqrt(cabs2(Hk[k])));
+  if ((est <= a.tol[s] && a.iters[s] >= a.miniters[s]) || a.iters[s] >= a.maxiters || happy) {
+    a.flag[s] = 0;
+    a.reorth[s] = 0;
+  } else {
+    a.scale[s * (m + 1) + k + 1] = 1.0 / beta;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_arn_step(ArnState a, const __grid_constant__ ArnJobs jb,
+                                                  const double2* __restrict__ part, int nblk,
+                                                  double2* __restrict__ coef, int pass, double eta2, int st2,
+                                                  int* __restrict__ host_flag) {
+  const int s = jb.ids[blockIdx.x];
+  const int m = a.m, k = jb.k;
+  if (!a.flag[s]) return;
+  const bool work = pass == 0 || a.reorth[s];
+  __shared__ double2 rows[130];
+  __shared__ double hred[8];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (work) {
+    for (int j = wid; j <= k + 1; j += 8) {  // one warp per row, fixed order
+      double2 v = czero();
+      const double2* pr = part + ((long long)s * st2 + j) * nblk;
+      for (int i = lane; i < nblk; i += 32) v = cadd(v, pr[i]);
+#pragma unroll
+      for (int d = 16; d > 0; d >>= 1) v = cadd(v, shfl_down2(v, d));
+      if (lane == 0) rows[j] = v;
+    }
+    __syncthreads();
+    double hs = 0.0;
+    for (int j = threadIdx.x; j <= k; j += blockDim.x) {
+      const double sc = a.scale[s * (m + 1) + j];
+      const double2 r = rows[j];
+      const double2 hj = make_double2(r.x * sc, r.y * sc);
+      double2* hp = a.h + s * (m + 1) + j;
+      *hp = pass == 0 ? hj : cadd(*hp, hj);
+      hs += cabs2(hj);
+      coef[(long long)s * st2 + j] = make_double2(-hj.x * sc, -hj.y * sc);
+    }
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) hs += __shfl_down_sync(0xffffffffu, hs, d);
+    if (lane == 0) hred[wid] = hs;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double hsum = 0.0;
+      for (int w8 = 0; w8 < 8; ++w8) hsum += hred[w8];
+      const double ww = rows[k + 1].x;
+      a.beta2[s] = ww - hsum;
+      if (!isfinite(ww) || !isfinite(hsum)) a.brk[s] = 1;
+      else if (pass == 0) a.reorth[s] = (ww - hsum < eta2 * ww) ? 1 : 0;
+    }
+  }
+  if (pass == 1 && threadIdx.x == 0) {
+    __threadfence_block();
+    arn_givens(a, s, k);
+    host_flag[s] = a.flag[s];  // mapped pinned memory: the host reads it after the step's event
   }
 }
 
@@ -158,6 +391,12 @@ static double dgks_eta2() {
   return v;
 }
 
+// Arnoldi recurrences on the host (default: one host round trip per Arnoldi step) or on the
+// device (IE_GMRES_DEVICE=1 when the context is created: look-ahead 1, no per-step round trip).  Measured on B200 (DESIGN.md
+// section 6): the device path is 3-12% SLOWER per iteration (c2mod 0.112 vs 0.101 ms, c3h 0.253
+// vs 0.225, c4h 0.705 vs 0.666, c5 6.27 vs 6.14): the always-launched DGKS second pass (two grids
+// of early-exiting CTAs) and the extra step kernel cost more than the ~20 us round trip they
+// remove.  Kept parity-tested, opt-in.
 // CTAs per system for the multi-dot kernel: ~2368 CTAs in total (16 per SM)
 static int dot_blocks(int nsys) { return std::max(32, std::min(1184, 2368 / std::max(1, nsys))); }
 
@@ -172,6 +411,16 @@ size_t gmres_scratch_bytes(int nx, int ny, int nz, int nsys, int restart) {
   add((size_t)nsys * (restart + 2) * nblk * sizeof(double2));           // partials
   add((size_t)nsys * (restart + 2) * sizeof(double2));                  // reduced rows
   add((size_t)nsys * (restart + 2) * sizeof(double2) + nsys * 64 * 2);  // jobs + coefficients
+  // device-side Arnoldi: H, cs, sn, g, scale, h, 10 per-system scalars, coefficients, rows, jobs
+  const size_t S = nsys, m = restart;
+  add(S * m * (m + 1) * sizeof(double2));
+  add(S * m * sizeof(double2));
+  add(S * m * sizeof(double2));
+  add(S * (m + 1) * sizeof(double2));
+  add(S * (m + 1) * sizeof(double));
+  add(S * (m + 1) * sizeof(double2));
+  for (int i = 0; i < 10; ++i) add(S * sizeof(double));
+  add(S * (m + 2) * sizeof(double2));
   add(4096);
   return b + 1024;
 }
@@ -242,6 +491,8 @@ ie_status gmres_batched(ie_ctx* c, Arena& ar, int nx, int ny, int nz, int k0, lo
   ap.mhat = gs->mhat;
   ap.X1 = scratch;
   ap.X2 = scratch + (size_t)items * 3 * 2 * N;
+  int devscale_k = -1;  // >= 0: the items' basis scale is read on the device (device-side Arnoldi)
+  ArnState* anp = nullptr;
   // apply to a list of (system, input, output) with given coefficients
   auto apply = [&](const std::vector<int>& ids, std::vector<const double2*> xin, std::vector<double> xsc,
                    std::vector<double2*> yout, double alpha, double beta, int acc) -> ie_status {
@@ -258,6 +509,7 @@ ie_status gmres_batched(ie_ctx* c, Arena& ar, int nx, int ny, int nz, int k0, lo
         it.dsig = sys[ids[b0 + i]].dsig;
         it.pm = sys[ids[b0 + i]].pm;
         it.xscale = xsc[b0 + i];
+        it.xscale_dev = (devscale_k >= 0 && anp) ? anp->scale + (size_t)ids[b0 + i] * (m + 1) + devscale_k : nullptr;
         it.sx0 = 0;
         it.sx1 = nx;
         it.sy0 = 0;
@@ -377,6 +629,165 @@ ie_status gmres_batched(ie_ctx* c, Arena& ar, int nx, int ny, int nz, int k0, lo
     }
   }
 
+  // ---- device-side Arnoldi (see k_arn_step); opt-in with IE_GMRES_DEVICE=1
+  const bool dev = c->gmres_device && S <= kMaxItems;  // ArnJobs holds <= kMaxItems live systems
+  ArnState an{};
+  anp = &an;
+  double2* d_coefs = nullptr;
+  const int st2 = m + 2;
+  if (dev) {
+    auto takeA = [&](size_t bytes) { return ar.take(bytes); };
+    an.H = (double2*)takeA((size_t)S * m * (m + 1) * sizeof(double2));
+    an.cs = (double2*)takeA((size_t)S * m * sizeof(double2));
+    an.sn = (double2*)takeA((size_t)S * m * sizeof(double2));
+    an.g = (double2*)takeA((size_t)S * (m + 1) * sizeof(double2));
+    an.scale = (double*)takeA((size_t)S * (m + 1) * sizeof(double));
+    an.h = (double2*)takeA((size_t)S * (m + 1) * sizeof(double2));
+    an.beta2 = (double*)takeA((size_t)S * sizeof(double));
+    an.bnorm = (double*)takeA((size_t)S * sizeof(double));
+    an.tol = (double*)takeA((size_t)S * sizeof(double));
+    an.est = (double*)takeA((size_t)S * sizeof(double));
+    an.flag = (int*)takeA((size_t)S * sizeof(int));
+    an.reorth = (int*)takeA((size_t)S * sizeof(int));
+    an.kdone = (int*)takeA((size_t)S * sizeof(int));
+    an.iters = (int*)takeA((size_t)S * sizeof(int));
+    an.miniters = (int*)takeA((size_t)S * sizeof(int));
+    an.brk = (int*)takeA((size_t)S * sizeof(int));
+    an.m = m;
+    an.maxiters = max_iters;
+    d_coefs = (double2*)takeA((size_t)S * st2 * sizeof(double2));
+    if (!an.H || !an.brk || !d_coefs)
+      return fail(c, IE_ERR_OUT_OF_MEMORY, "workspace too small for GMRES (need " + std::to_string(ar.peak) +
+                                               " bytes; see ie_workspace_query)");
+    const size_t hbytes = (size_t)m * S * sizeof(int) + 256;
+    if (c->h_arn_cap < hbytes) {
+      if (c->h_arnflag) cudaFreeHost(c->h_arnflag);
+      c->h_arnflag = nullptr;
+      IE_CUDA(c, cudaHostAlloc((void**)&c->h_arnflag, hbytes, cudaHostAllocMapped));
+      IE_CUDA(c, cudaHostGetDevicePointer((void**)&c->d_arnflag, c->h_arnflag, 0));
+      c->h_arn_cap = hbytes;
+    }
+    if (c->ev_arn.size() < (size_t)m) {
+      while (c->ev_arn.size() < (size_t)m) {
+        cudaEvent_t ev;
+        IE_CUDA(c, cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        c->ev_arn.push_back(ev);
+      }
+    }
+    std::vector<double> tolv(S), bn(S);
+    std::vector<int> mi(S);
+    for (int s2 = 0; s2 < S; ++s2) {
+      tolv[s2] = sys[s2].tol;
+      bn[s2] = ss[s2].bnorm;
+      mi[s2] = sys[s2].min_iters;
+    }
+    IE_CUDA(c, cudaMemcpyAsync(an.tol, tolv.data(), S * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    IE_CUDA(c, cudaMemcpyAsync(an.bnorm, bn.data(), S * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    IE_CUDA(c, cudaMemcpyAsync(an.miniters, mi.data(), S * sizeof(int), cudaMemcpyHostToDevice, c->stream));
+    IE_CUDA(c, cudaMemsetAsync(an.brk, 0, S * sizeof(int), c->stream));
+    IE_CUDA(c, cudaStreamSynchronize(c->stream));  // the host vectors above go out of scope
+  }
+  // one GMRES cycle with the recurrences on the device for the systems `act`
+  auto device_cycle = [&](const std::vector<int>& act) -> ie_status {
+    const int n = (int)act.size();
+    {  // cycle start: scale_0 = 1/beta, g = (beta, 0, ...), flag = 1, kdone = 0, iters = host count
+      std::vector<double> sc0(S, 0.0);
+      std::vector<double2> g0((size_t)S * (m + 1), make_double2(0.0, 0.0));
+      std::vector<int> fl(S, 0), it0(S, 0);
+      for (int s2 = 0; s2 < S; ++s2) it0[s2] = res[s2].iters;
+      for (int s2 : act) {
+        sc0[s2] = 1.0 / ss[s2].beta;
+        g0[(size_t)s2 * (m + 1)] = make_double2(ss[s2].beta, 0.0);
+        fl[s2] = 1;
+      }
+      IE_CUDA(c, cudaMemcpy2DAsync(an.scale, (m + 1) * sizeof(double), sc0.data(), sizeof(double), sizeof(double), S,
+                                   cudaMemcpyHostToDevice, c->stream));
+      IE_CUDA(c, cudaMemcpyAsync(an.g, g0.data(), g0.size() * sizeof(double2), cudaMemcpyHostToDevice, c->stream));
+      IE_CUDA(c, cudaMemcpyAsync(an.flag, fl.data(), S * sizeof(int), cudaMemcpyHostToDevice, c->stream));
+      IE_CUDA(c, cudaMemcpyAsync(an.iters, it0.data(), S * sizeof(int), cudaMemcpyHostToDevice, c->stream));
+      IE_CUDA(c, cudaMemsetAsync(an.kdone, 0, S * sizeof(int), c->stream));
+      IE_CUDA(c, cudaMemsetAsync(an.reorth, 0, S * sizeof(int), c->stream));
+      IE_CUDA(c, cudaStreamSynchronize(c->stream));  // the staging vectors go out of scope
+    }
+    int* hflags = c->h_arnflag;  // mapped pinned [m][S], written by k_arn_step
+    int* hflags_dev = c->d_arnflag;
+    for (size_t i = 0; i < (size_t)m * S; ++i) hflags[i] = 1;
+    std::vector<int> live = act;
+    for (int k = 0; k < m && !live.empty(); ++k) {
+      // w = A v_k (basis scale read on the device)
+      std::vector<const double2*> xin;
+      std::vector<double> xsc;
+      std::vector<double2*> yo;
+      for (int s2 : live) {
+        xin.push_back(Vs(s2, k));
+        xsc.push_back(1.0);
+        yo.push_back(Vs(s2, k + 1));
+      }
+      devscale_k = k;
+      ie_status sa = apply(live, xin, xsc, yo, 1.0, -1.0, 0);
+      devscale_k = -1;
+      if (sa) return sa;
+      const int nl = (int)live.size();
+      ArnJobs jb{};
+      jb.V = V;
+      jb.sys_stride = (long long)(m + 1) * len;
+      jb.len = len;
+      jb.k = k;
+      jb.nlive = nl;
+      for (int i = 0; i < nl; ++i) jb.ids[i] = live[i];
+      const int gx = (int)std::max<long long>(1, std::min<long long>((len + 255) / 256, 1184 / nl + 1));
+      for (int pass = 0; pass < 2; ++pass) {
+        jb.enable = pass == 0 ? an.flag : an.reorth;
+        k_mdot_arn<kDotG><<<dim3(nblk, (k + 1) / kDotG + 1, nl), 256, 0, c->stream>>>(jb, part, nblk, st2);
+        IE_CHECK_LAUNCH(c, "k_mdot_arn");
+        k_arn_step<<<nl, 256, 0, c->stream>>>(an, jb, part, nblk, d_coefs, pass, dgks_eta2(), st2,
+                                               hflags_dev + (size_t)k * S);
+        IE_CHECK_LAUNCH(c, "k_arn_step");
+        k_maxpy_arn<<<dim3(gx, nl), 256, 0, c->stream>>>(jb, d_coefs, st2);
+        IE_CHECK_LAUNCH(c, "k_maxpy_arn");
+      }
+      IE_CUDA(c, cudaEventRecord(c->ev_arn[k], c->stream));
+      if (k >= 1) {  // look-ahead 1: the flags of step k-1 decide step k+1
+        IE_CUDA(c, cudaEventSynchronize(c->ev_arn[k - 1]));
+        std::vector<int> nxt;
+        for (int s2 : live)
+          if (hflags[(size_t)(k - 1) * S + s2]) nxt.push_back(s2);
+        live.swap(nxt);
+      }
+    }
+    IE_CUDA(c, cudaStreamSynchronize(c->stream));
+    // the cycle's recurrences back to the host (the end-of-cycle update below uses them)
+    std::vector<double2> Hh((size_t)S * m * (m + 1)), gh((size_t)S * (m + 1));
+    std::vector<double> sch((size_t)S * (m + 1)), esth(S);
+    std::vector<int> kd(S), ith(S), bk(S);
+    IE_CUDA(c, cudaMemcpy(Hh.data(), an.H, Hh.size() * sizeof(double2), cudaMemcpyDeviceToHost));
+    IE_CUDA(c, cudaMemcpy(gh.data(), an.g, gh.size() * sizeof(double2), cudaMemcpyDeviceToHost));
+    IE_CUDA(c, cudaMemcpy(sch.data(), an.scale, sch.size() * sizeof(double), cudaMemcpyDeviceToHost));
+    IE_CUDA(c, cudaMemcpy(esth.data(), an.est, S * sizeof(double), cudaMemcpyDeviceToHost));
+    IE_CUDA(c, cudaMemcpy(kd.data(), an.kdone, S * sizeof(int), cudaMemcpyDeviceToHost));
+    IE_CUDA(c, cudaMemcpy(ith.data(), an.iters, S * sizeof(int), cudaMemcpyDeviceToHost));
+    IE_CUDA(c, cudaMemcpy(bk.data(), an.brk, S * sizeof(int), cudaMemcpyDeviceToHost));
+    for (int s2 : act) {
+      SysState& q = ss[s2];
+      q.k = kd[s2];
+      for (int kk = 0; kk < q.k; ++kk)
+        for (int j = 0; j <= kk + 1; ++j) {
+          const double2 v = Hh[((size_t)s2 * m + kk) * (m + 1) + j];
+          q.H[(size_t)kk * (m + 1) + j] = cplx(v.x, v.y);
+        }
+      for (int j = 0; j <= q.k; ++j) q.g[j] = cplx(gh[(size_t)s2 * (m + 1) + j].x, gh[(size_t)s2 * (m + 1) + j].y);
+      for (int j = 0; j < q.k; ++j) q.scale[j] = sch[(size_t)s2 * (m + 1) + j];
+      res[s2].iters = ith[s2];
+      if (q.k > 0) res[s2].relres_est = esth[s2];
+      if (bk[s2]) {
+        res[s2].breakdown = 1;
+        q.active = false;
+      }
+      q.cycle = false;
+    }
+    return IE_OK;
+  };
+
   while (true) {
     std::vector<int> act;
     for (int s = 0; s < S; ++s)
@@ -390,7 +801,11 @@ ie_status gmres_batched(ie_ctx* c, Arena& ar, int nx, int ny, int nz, int k0, lo
       q.k = 0;
       q.cycle = true;
     }
-    for (int k = 0; k < m; ++k) {
+    if (dev) {  // ---- device-side recurrences: no host round trip per Arnoldi step
+      st = device_cycle(act);
+      if (st) return st;
+    }
+    for (int k = 0; k < (dev ? 0 : m); ++k) {
       std::vector<int> it;
       for (int s : act)
         if (ss[s].cycle) it.push_back(s);

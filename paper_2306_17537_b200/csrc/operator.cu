@@ -45,7 +45,7 @@ __global__ void __launch_bounds__(128, 5) k_xfwd(const __grid_constant__ ApplyPa
   const long long sN = (long long)sbx * sby * sbz;
   const double2* xrow = it.x + ((long long)(zz - it.sz0) * sby + (yy - it.sy0)) * sbx - it.sx0;
   const double* srow = it.dsig + zz * p.ds_zs + yy * p.ds_ys;
-  const double xs = it.xscale;
+  const double xs = item_xscale(it);
 
   // J for the thread's (non-zero) first-stage inputs, then one line FFT per component (a
   // thread holds 3 x V/2 values of J plus the V values of the line in flight)
@@ -683,7 +683,7 @@ __global__ void __launch_bounds__(128) k_xinv(const __grid_constant__ ApplyParam
   fft_run<L, false, +1, 1, false, true>(v, sm, idx, t, p.tw_x, false);
   if (!valid) return;
   const long long off = ((long long)zz * ny + yy) * nx;
-  const double a = p.alpha * it.xscale, b = p.beta;
+  const double a = p.alpha * item_xscale(it), b = p.beta;
   double2* yrow = it.y + l * N + off;
   const double2* xrow = it.x + l * N + off;
   // contraction-IE right preconditioner: the identity term is (P x)_l (row l of sym6 P)
@@ -846,7 +846,7 @@ __global__ void __launch_bounds__(FusedShape<LY>::NT, 1024 / FusedShape<LY>::NT)
       if (valid) {
         const int zz = z;
         const long long off = ((long long)zz * ny + yy) * nx;
-        const double al = p.alpha * it.xscale, be = p.beta;
+        const double al = p.alpha * item_xscale(it), be = p.beta;
         double2* yrow = it.y + l * N + off;
         const double2* xrow = it.x + l * N + off;
         const int pc0 = l == 0 ? 0 : (l == 1 ? 3 : 4), pc1 = l == 0 ? 3 : (l == 1 ? 1 : 5),
@@ -944,7 +944,7 @@ __global__ void __launch_bounds__(FusedShape<LY>::NT, 512 / FusedShape<LY>::NT) 
       const long long sN = (long long)sbx * sby * sbz;
       const double2* xrow = it.x + ((long long)(zz - it.sz0) * sby + (yy - it.sy0)) * sbx - it.sx0;
       const double* srow = it.dsig + zz * p.ds_zs + yy * p.ds_ys;
-      const double xs = it.xscale;
+      const double xs = item_xscale(it);
       double2 J[3][VX / 2];
 #pragma unroll
       for (int u = 0; u < VX / R0X; ++u)

@@ -292,3 +292,29 @@ def test_warm_start_and_preconditioner_calls(scheme):
     ie.ie_set_preconditioner(ctx, 1)
     st4 = ie.ie_solve_dd(ctx, e, scheme, boxes=cfg.boxes, outer_tol=1e-10, restart=30, max_sweeps=300, precond=1)
     assert rel(e.cpu().numpy(), X) < FIELD_TOL and st4["e_final"] <= 1e-10
+
+
+@pytest.mark.parametrize("name,scheme,precond", [("c2mini", "full", 0), ("c2mini", "jacobi", 1),
+                                                 ("c5mini", "gauss_seidel", 0), ("c3mini", "fgmres_jacobi", 0)])
+def test_device_side_arnoldi_matches_dense_lu(name, scheme, precond):
+    """The opt-in device-side Arnoldi recurrences (IE_GMRES_DEVICE=1 at context creation: Hessenberg
+    column, DGKS test, Givens rotations and stop rule on the device, look-ahead 1) reach the same
+    solution as dense LU; iteration counts within one per solve of the host-recurrence path."""
+    import os
+    import paper_2306_17537_b200 as ie
+    cfg = make_config(name)
+    out = []
+    for dev in ("1", "0"):
+        os.environ["IE_GMRES_DEVICE"] = dev
+        try:
+            ctx, sigma = gpu_ctx(cfg)
+        finally:
+            os.environ.pop("IE_GMRES_DEVICE", None)
+        k0, ds, E0, X = _lu_truth(cfg, sigma)
+        e = _field(cfg, len(E0))
+        st = ie.ie_solve_dd(ctx, e, scheme, boxes=cfg.boxes, outer_tol=1e-10, restart=30, max_sweeps=300,
+                            inner_tol_fixed=1e-2 if scheme.startswith("fgmres") else 1e-6, precond=precond)
+        assert st["e_final"] <= 1e-10
+        assert rel(e.cpu().numpy(), X) < FIELD_TOL
+        out.append(st)
+    assert abs(out[0]["total_inner_iters"] - out[1]["total_inner_iters"]) <= max(2, out[1]["total_inner_iters"] // 50)
