@@ -392,11 +392,12 @@ static double dgks_eta2() {
 }
 
 // Arnoldi recurrences on the host (default: one host round trip per Arnoldi step) or on the
-// device (IE_GMRES_DEVICE=1 when the context is created: look-ahead 1, no per-step round trip).  Measured on B200 (DESIGN.md
-// section 6): the device path is 3-12% SLOWER per iteration (c2mod 0.112 vs 0.101 ms, c3h 0.253
-// vs 0.225, c4h 0.705 vs 0.666, c5 6.27 vs 6.14): the always-launched DGKS second pass (two grids
-// of early-exiting CTAs) and the extra step kernel cost more than the ~20 us round trip they
-// remove.  Kept parity-tested, opt-in.
+// device (IE_GMRES_DEVICE=1 when the context is created: look-ahead 1, no per-step round trip).
+// Measured on B200: the device path is 3-12% SLOWER per iteration (c2mod
+// 0.112 vs 0.101 ms, c3h 0.253 vs 0.225, c4h 0.705 vs 0.666, c5 6.27 vs 6.14): the
+// always-launched DGKS second pass (two grids of early-exiting CTAs) and the extra step kernel
+// cost more than the ~20 us round trip they remove.  Kept parity-tested, opt-in.
+
 // CTAs per system for the multi-dot kernel: ~2368 CTAs in total (16 per SM)
 static int dot_blocks(int nsys) { return std::max(32, std::min(1184, 2368 / std::max(1, nsys))); }
 
