@@ -4,7 +4,7 @@ north_star: operator to rel-L2 <= 1e-12, fields and receiver voltages <= 1e-6 at
 * the operator, element by element over the whole grid, vs the oracle's Eq. 10 FFT convolution
   (oracle.operator.Operator, scipy.fft on all host cores);
 * the solves: the oracle's restarted GMRES with the contraction-IE right preconditioner
-  (oracle/preconditioner.py, pinned) to 1e-11 is the truth (three orders below the GPU's 1e-9); the GPU's full-domain GMRES, GS-A and
+  (oracle/preconditioner.py, pinned) to 1e-10 is the truth (an order below the GPU's 1e-9); the GPU's full-domain GMRES, GS-A and
   FGMRES-Jacobi at tol 1e-9 must match it in the fields and receiver H / voltages, and DD must
   agree with the full-domain solve (section 3.1).
 Marked slow: the oracle solve takes several minutes on the box's host cores."""
@@ -45,7 +45,7 @@ def test_c5_operator_elementwise(c5):
 
 @pytest.fixture(scope="module")
 def c5_truth(c5):
-    """Oracle solution at tol 1e-11 (contraction-IE right-preconditioned GMRES: same system, same
+    """Oracle solution at tol 1e-10 (contraction-IE right-preconditioned GMRES: same system, same
     Eq. 9 residual) and its receiver fields."""
     cfg, sigma, k0, ds, A = c5
     pts = physics.centroids(cfg.n, cfg.hvec, cfg.origin)
@@ -53,7 +53,7 @@ def c5_truth(c5):
     E0 = np.ascontiguousarray(np.moveaxis(physics.incident_E(pts, src, m, k0, cfg.freq), -1, 0))
     del pts
     P = pc.contraction_P(sigma, cfg.sigma_b)
-    chi, info = gmres.gmres(lambda c: A(pc.apply_cellwise(P, c)), E0, tol=1e-11, restart=30, max_iters=400)
+    chi, info = gmres.gmres(lambda c: A(pc.apply_cellwise(P, c)), E0, tol=1e-10, restart=20, max_iters=400)
     assert info["converged"], info["relres_true"]
     E = pc.apply_cellwise(P, chi)
     H = receivers.receiver_H(cfg.n, cfg.hvec, cfg.origin, k0, cfg.sigma_b, ds, E, cfg.receivers, src, m)
