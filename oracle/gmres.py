@@ -48,7 +48,7 @@ def gmres(A, b, x0=None, tol=1e-9, restart=30, max_iters=5000, min_iters=0):
             info["iters"] += 1
             for j in range(k + 1):  # modified Gram-Schmidt
                 H[j, k] = _dot(V[j], w)
-                w = w - H[j, k] * V[j]
+                w -= H[j, k] * V[j]
             H[k + 1, k] = _nrm(w)
             # apply previous rotations to the new column
             for j in range(k):
@@ -80,7 +80,7 @@ def gmres(A, b, x0=None, tol=1e-9, restart=30, max_iters=5000, min_iters=0):
         # least squares: H[:k,:k] y = g[:k]
         y = np.linalg.solve(np.triu(H[:k_done, :k_done]), g[:k_done])
         for j in range(k_done):
-            x = x + y[j] * V[j]
+            x += y[j] * V[j]
         r = b - A(x)
         beta = _nrm(r)
         info["relres_true"] = beta / bnorm
