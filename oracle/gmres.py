@@ -45,6 +45,8 @@ def gmres(A, b, x0=None, tol=1e-9, restart=30, max_iters=5000, min_iters=0):
         done = False
         for k in range(m):
             w = A(V[k])
+            if np.may_share_memory(w, V[k]):  # w is updated in place below
+                w = w.copy()
             info["iters"] += 1
             for j in range(k + 1):  # modified Gram-Schmidt
                 H[j, k] = _dot(V[j], w)
