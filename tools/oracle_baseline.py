@@ -84,4 +84,35 @@ try:
             print(json.dumps(out["runs"][-1]), flush=True)
 except Exception as exc:  # no GPU here: the oracle timings stand alone
     out["gpu_error"] = repr(exc)
-json.dump(out, open(sys.argv[1] if len(sys.argv) > 1 else "profiles/r02_oracle_solves.json", "w"), indent=1)
+if "--c4" in sys.argv:
+    # one c4mid station (31, 400 kHz, 3 RHS) with the physical table: oracle layered operator
+    # (2-D FFT + dense z contraction) + GMRES(30) with the contraction IE, tol 1e-6
+    from ie_workloads import layered_inputs as li
+    from oracle import layered as lay
+    cfg = make_config("c4mid")
+    med = li.medium(cfg)
+    t0 = time.perf_counter()
+    T = li.table(cfg, med)
+    t_table = time.perf_counter() - t0
+    sig = cfg.sigma()
+    sbz = lay.background_per_layer(cfg.n, cfg.origin, cfg.hvec, *cfg.background())
+    dsl = lay.contrast_layered(sig, sbz)
+    t0 = time.perf_counter()
+    Al = lay.LayeredOperator(T, dsl)
+    t_setup = time.perf_counter() - t0
+    del T
+    E0s = li.incident(cfg, med)
+    Pl = pc.contraction_P(sig, np.broadcast_to(sbz[:, None, None], sig.shape[:3]))
+    t0 = time.perf_counter()
+    its = []
+    for r in range(len(E0s)):
+        chi, info = gmres.gmres(lambda c_: Al(pc.apply_cellwise(Pl, c_)), E0s[r], tol=cfg.outer_tol, restart=30,
+                                max_iters=400)
+        its.append(info["iters"])
+    out["runs"].append({"workload": "c4mid station 31, 400 kHz, 3 RHS: oracle layered GMRES(30) + CIE, tol 1e-6",
+                        "table_s": round(t_table, 1), "setup_s": round(t_setup, 1),
+                        "solve_s": round(time.perf_counter() - t0, 1), "iters": its,
+                        "gpu_same_solve_s": "c4 sweep c4mid@1e-06:full_gmres_cie per (station, frequency) unit"})
+    print(json.dumps(out["runs"][-1]), flush=True)
+json.dump(out, open(sys.argv[1] if len(sys.argv) > 1 and not sys.argv[1].startswith("--") else
+                    "profiles/r02_oracle_solves.json", "w"), indent=1)
