@@ -496,6 +496,29 @@ def c4_layered_units(units, variants=C4_VARIANTS, verbose=False, rank=0, ws=1, a
         info["setup_s"][str(f)] = round(time.perf_counter() - t0, 3)
         del T
         fut = pool.submit(gen, med, mine[0][1])
+        if "operator" not in info:  # the layered c4-grid operator, 3 RHS, per-kernel (A3L K-C')
+            nx, ny, nz = cfg.n
+            xo = torch.randn((3, 3, nz, ny, nx), dtype=torch.complex128, device="cuda")
+            yo = torch.empty_like(xo)
+            for _ in range(2):
+                ie.ie_apply_operator(ctx, xo, yo)
+            ie.ie_profile(ctx, True)
+            for _ in range(5):
+                ie.ie_apply_operator(ctx, xo, yo)
+            prof = ie.ie_profile_read(ctx)
+            ie.ie_profile(ctx, False)
+            R = 3 * nz
+            kc = prof["K-C z-convolution"]
+            kc_ms = kc[0] / max(1, kc[1])
+            flops = 8 * R * R * 4 * nx * ny * 3
+            table = (nx + 1) * (ny + 1) * R * R * 16
+            info["operator"] = {"workload": f"c4 grid layered operator, physical table, 3 RHS, {f:g} Hz",
+                                "ms_per_apply": round(sum(v[0] for v in prof.values()) / 5, 4),
+                                "kernels_ms": {k: round(v[0] / v[1], 4) for k, v in prof.items() if v[1] > 0},
+                                "k_c_prime": {"ms": round(kc_ms, 4), "fp64_tflops": round(flops / kc_ms / 1e9, 2),
+                                              "table_gbs": round(table / kc_ms / 1e6, 1),
+                                              "pipe": "DMMA m8n8k4 f64 (tensor cores)"}}
+            del xo, yo
         for i, u in enumerate(mine):
             E0, e0rx, h0, g = fut.result()
             info["gen_s"].append(g)
@@ -537,7 +560,8 @@ def c4_layered_sweep(stations=(0, 31, 63), freqs=(4e5,), variants=C4_VARIANTS, v
            "generation_s_per_unit": round(float(np.mean(gens)), 2) if gens else None,
            "generation": "host (layered_green): E0 of the 3 transmitter dipoles + 9 receiver dipoles per unit, "
                          "overlapped with the previous unit's GPU work; excluded from s/position",
-           "rank_wall_s": round(wall, 2)}
+           "rank_wall_s": round(wall, 2),
+           "operator": next((v["operator"] for v in infos.values() if "operator" in v), None)}
     for name, tol, runs in variants:
         for scheme, pc in runs:
             k = _run_key(name, tol, scheme, pc)
