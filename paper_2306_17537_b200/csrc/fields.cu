@@ -52,7 +52,9 @@ __global__ void k_contrast_sym6(const double* __restrict__ s, double* __restrict
 
 ie_status pack_contrast(ie_ctx* c, const void* sigma_dev, int layout) {
   const long long N = (long long)c->g.nx * c->g.ny * c->g.nz;
-  if (!c->dsig) IE_CUDA(c, cudaMalloc(&c->dsig, 6 * N * sizeof(double)));
+  // pack into a fresh buffer: a rejected conductivity leaves the context's contrast untouched
+  double* dnew = nullptr;
+  IE_CUDA(c, cudaMalloc(&dnew, 6 * N * sizeof(double)));
   int* bad = nullptr;
   double* sbz = nullptr;  // per-layer background (P:48 with sigma_b(z); reading R17)
   IE_CUDA(c, cudaMalloc(&bad, 8 + (c->layered ? c->g.nz * sizeof(double) : 0)));
@@ -65,10 +67,10 @@ ie_status pack_contrast(ie_ctx* c, const void* sigma_dev, int layout) {
   }
   const long long nxy = (long long)c->g.nx * c->g.ny;
   if (layout == 0)
-    k_contrast_full9<<<grid_for(N, 256), 256, 0, c->stream>>>((const double*)sigma_dev, c->dsig, N, c->sigma_b, sbz,
+    k_contrast_full9<<<grid_for(N, 256), 256, 0, c->stream>>>((const double*)sigma_dev, dnew, N, c->sigma_b, sbz,
                                                               nxy, bad);
   else
-    k_contrast_sym6<<<grid_for(N, 256), 256, 0, c->stream>>>((const double*)sigma_dev, c->dsig, N, c->sigma_b, sbz,
+    k_contrast_sym6<<<grid_for(N, 256), 256, 0, c->stream>>>((const double*)sigma_dev, dnew, N, c->sigma_b, sbz,
                                                              nxy, bad);
   c->launches++;
   int hbad = 0;
@@ -76,8 +78,11 @@ ie_status pack_contrast(ie_ctx* c, const void* sigma_dev, int layout) {
   if (!e) e = cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, c->stream);
   if (!e) e = cudaStreamSynchronize(c->stream);
   cudaFree(bad);
+  if (e || hbad) cudaFree(dnew);
   if (e) return cuda_fail(c, e, "set_contrast");
   if (hbad) return fail(c, IE_ERR_INVALID_ARGUMENT, "sigma is not symmetric to 1e-12 (P:415) or not finite");
+  cudaFree(c->dsig);
+  c->dsig = dnew;
   c->contrast_set = true;
   if (c->pre_p) {  // a new contrast invalidates the preconditioner (rebuilt on next use)
     cudaFree(c->pre_p);

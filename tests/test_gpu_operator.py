@@ -170,3 +170,58 @@ def test_zpass_variants_match_oracle(env):
                         os.path.abspath(__file__) + "::test_apply_operator_matches_oracle"],
                        env=dict(os.environ, **{k: v}), capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+
+
+def test_abi_error_contract():
+    """The C-ABI's documented error behaviour (include/ie_b200.h): call-order
+    violations return IE_ERR_STATE, a too-small workspace IE_ERR_OUT_OF_MEMORY with the required
+    bytes in the message, a non-partition box set and an unsymmetric or non-finite conductivity
+    IE_ERR_INVALID_ARGUMENT, a non-finite right-hand side IE_ERR_BREAKDOWN from the solver, a
+    layered-only call on a homogeneous context IE_ERR_STATE; no call aborts the process."""
+    import torch
+    import paper_2306_17537_b200 as ie
+    cfg = make_config("c2mini")
+    nx, ny, nz = cfg.n
+    ctx = ie.ie_create(cfg.n, cfg.hvec, cfg.origin, cfg.sigma_b, cfg.freq)
+    x = torch.zeros((1, 3, nz, ny, nx), dtype=torch.complex128, device="cuda")
+    y = torch.empty_like(x)
+    with pytest.raises(ie.IEError) as e:  # no contrast yet
+        ie.ie_apply_operator(ctx, x, y)
+    assert e.value.status == 6
+    ws = torch.empty(1024, dtype=torch.uint8, device="cuda")
+    ie.ie_bind_workspace(ctx, ws)
+    sigma = cfg.sigma()
+    ie.ie_set_contrast(ctx, torch.from_numpy(sigma).cuda())
+    with pytest.raises(ie.IEError) as e:  # workspace too small
+        ie.ie_apply_operator(ctx, x, y)
+    assert e.value.status == 2 and "need" in str(e.value)
+    ie.ensure_workspace(ctx, boxes=cfg.boxes, nrhs=1, restart=30)
+    with pytest.raises(ie.IEError) as e:  # no sources
+        ie.ie_solve_dd(ctx, x, "full")
+    assert e.value.status == 6
+    ie.ie_set_source(ctx, np.array([cfg.sources[0][0]]), np.array([cfg.sources[0][1]]))
+    with pytest.raises(ie.IEError) as e:  # boxes that overlap
+        ie.ie_solve_dd(ctx, x, "jacobi", boxes=[(0, 8, 0, 8, 0, 5), (0, 8, 0, 8, 4, 8)])
+    assert e.value.status == 1
+    with pytest.raises(ie.IEError) as e:  # homogeneous context has no layered spectrum
+        ie.ie_get_layer_spectrum(ctx)
+    assert e.value.status == 6
+    bad = sigma.copy()
+    bad[0, 0, 0, 0, 1] += 0.5  # unsymmetric tensor
+    with pytest.raises(ie.IEError) as e:
+        ie.ie_set_contrast(ctx, torch.from_numpy(bad).cuda())
+    assert e.value.status == 1
+    nan = sigma.copy()
+    nan[3, 3, 3] = np.nan
+    with pytest.raises(ie.IEError) as e:  # non-finite conductivity rejected at the boundary
+        ie.ie_set_contrast(ctx, torch.from_numpy(nan).cuda())
+    assert e.value.status == 1
+    e0 = torch.empty_like(x)
+    ie.ie_get_incident(ctx, e0)
+    e0[0, 1, 2, 3, 4] = float("nan")  # a non-finite right-hand side: the solver reports breakdown
+    ie.ie_set_incident(ctx, e0)
+    st = ie.ie_solve_dd(ctx, x, "full", outer_tol=1e-8, check=False)
+    assert st["status"] == 5  # IE_ERR_BREAKDOWN
+    ie.ie_set_source(ctx, np.array([cfg.sources[0][0]]), np.array([cfg.sources[0][1]]))  # recovers
+    st = ie.ie_solve_dd(ctx, x, "full", outer_tol=1e-8)
+    assert st["e_final"] <= 1e-8
