@@ -434,7 +434,8 @@ def shared_table(cfg, med, rank=0, ws=1):
     import torch.distributed as dist
     from threadpoolctl import threadpool_limits
     nx, ny, nz = cfg.n
-    buf = torch.empty((3, 3, nz, nz, ny, nx), dtype=torch.complex128, device="cuda")
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    buf = torch.empty((3, 3, nz, nz, ny, nx), dtype=torch.complex128, device=dev)
     T = None
     if rank == 0:
         with threadpool_limits(len(os.sched_getaffinity(0))):
@@ -444,7 +445,8 @@ def shared_table(cfg, med, rank=0, ws=1):
     if T is None:
         T = buf.cpu().numpy()
     del buf
-    torch.cuda.empty_cache()
+    if dev == "cuda":
+        torch.cuda.empty_cache()
     return T
 
 

@@ -123,3 +123,40 @@ def test_distributed_sweep_solves_each_unit_once_and_merges_like_one_rank():
     for u in units:
         assert np.array_equal(np.array(out[0][2][u]), single[u])
         assert np.array_equal(np.array(out[1][2][u]), single[u])
+
+
+def _table_worker(rank, ws, port, q):
+    import sys
+    import numpy as np
+    import torch.distributed as dist
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import bench
+    from ie_workloads import make_config, layered_inputs as li
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=ws)
+    cfg = make_config("c3lmini")
+    T = bench.shared_table(cfg, li.medium(cfg), rank, ws)
+    q.put((rank, T))
+    dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+def test_shared_table_is_generated_once_and_broadcast():
+    """N > 1 ranks: rank 0 generates the layered table, the others receive it by broadcast --
+    identical bytes on every rank, equal to a local generation."""
+    import sys
+    import numpy as np
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from ie_workloads import make_config, layered_inputs as li
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_table_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    out = dict(q.get(timeout=250) for _ in ps)
+    for p in ps:
+        p.join(timeout=30)
+    cfg = make_config("c3lmini")
+    ref = li.table(cfg, li.medium(cfg))
+    assert np.array_equal(out[0], ref) and np.array_equal(out[1], ref)
