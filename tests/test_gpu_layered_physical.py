@@ -6,9 +6,9 @@ inputs from ie_workloads.layered_green (input data, pinned in tests/test_layered
   schemes and the contraction-IE variant vs the oracle's dense LU of the layered system (R17),
   fields <= 1e-6 at solver tolerance 1e-9, receiver couplings by reciprocity vs the oracle;
 * the literal c3 mini (contrast up to 500 in the 0.01 S/m layer, cond ~4e4): operator parity;
-* full size (c3 64^3, c4 128x128x64): the operator at sampled output cells vs the oracle's direct
-  layered sum, and c3capped solves (full vs GS-A, fields and receivers agree; residual at sampled
-  cells by the oracle)."""
+* full size: the c3 operator element by element vs the oracle's LayeredOperator; c3 and c4 at
+  sampled output cells vs the oracle's direct layered sum; c3capped and c4mid solves (full vs
+  GS-A, fields and receivers agree; residual at sampled cells by the oracle)."""
 
 import numpy as np
 import pytest
