@@ -634,60 +634,6 @@ def moving_window(n_stations=5, n=(256, 128, 128), h=0.25, splits=(2, 1, 1), sch
 C4_FREQS = (1e5, 4e5, 2e6)
 
 
-def c4_sweep(stations=(0, 31, 63), schemes=("full", "gauss_seidel"), outer_tol=1e-6, restart=30, verbose=False):
-    """c4 deviated-well logging sweep (BASELINE.json configs[3]) on the homogeneous stand-in
-    background c4h (sigma_b = 0.01 S/m, the middle layer; the layered table is DESIGN R19): one
-    context per frequency (Green setup amortised over the stations, excluded from s/position,
-    SURVEY 8(d)), triaxial source = 3 RHS, receivers at 1, 3, 7 m; s/position = E0 + solve +
-    receivers summed over the 3 frequencies."""
-    import torch
-    import paper_2306_17537_b200 as ie
-    from ie_workloads import make_config
-    from ie_workloads.configs import c4_stations
-    cfg = make_config("c4h")
-    sigma = torch.from_numpy(cfg.sigma()).cuda()
-    st = c4_stations()
-    nx, ny, nz = cfg.n
-    ctxs = {}
-    t0 = time.perf_counter()
-    for f in C4_FREQS:
-        c = ie.ie_create(cfg.n, cfg.hvec, cfg.origin, cfg.sigma_b, f)
-        ie.ensure_workspace(c, boxes=cfg.boxes, nrhs=3, restart=restart)
-        ie.ie_set_contrast(c, sigma)
-        ctxs[f] = c
-    torch.cuda.synchronize()
-    setup_s = time.perf_counter() - t0
-    e = torch.empty((3, 3, nz, ny, nx), dtype=torch.complex128, device="cuda")
-    out = {"workload": "c4h sweep (128x128x64, 3 freqs x 3 dipoles, rx 1/3/7 m)", "setup_s": round(setup_s, 3),
-           "stations": list(stations), "outer_tol": outer_tol, "restart": restart}
-    for scheme in schemes:
-        per_pos, iters, status = [], [], []
-        for s in stations:
-            ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            torch.cuda.synchronize()
-            ev0.record()
-            its = 0
-            for f in C4_FREQS:
-                c = ctxs[f]
-                ie.ie_set_source(c, np.repeat(st[s]["tx"][None], 3, 0), st[s]["moments"])
-                r = ie.ie_solve_dd(c, e, scheme, boxes=cfg.boxes, outer_tol=outer_tol, restart=restart,
-                                   max_sweeps=100, max_iters=3000, check=False)
-                ie.ie_receiver_fields(c, e, st[s]["rx"])
-                its += r["total_inner_iters"]
-                status.append(ie.STATUS.get(r["status"], r["status"]))
-                if verbose:
-                    print(scheme, s, f, r["total_inner_iters"], r["sweeps"], r["e_final"], status[-1], flush=True)
-            ev1.record()
-            torch.cuda.synchronize()
-            per_pos.append(ev0.elapsed_time(ev1) / 1e3)
-            iters.append(its)
-        out[scheme] = {"s_per_position": round(float(np.mean(per_pos)), 4), "per_station_s": [round(x, 4) for x in per_pos],
-                       "gmres_iters_per_station": iters, "status": sorted(set(status))}
-    return out
-
-
-
-
 def operator_leg(name="c4h", steps=20):
     """The homogeneous operator (K-A..K-E) on another grid of the suite: SURVEY 8(d) judges the >=60%
     HBM target on c5 AND on the c4 grid (128x128x64) with a homogeneous background.  Device-resident
