@@ -227,9 +227,13 @@ def gl_nodes(kmax, width, order=_GL_ORDER, zeta_max=None, kim_min=None):
 
 
 def radial_nodes(rho_max, h, seg_len=2.0, n_near=16, n_far=20):
-    """Piecewise Chebyshev-Lobatto nodes in rho: [0,h],[h,2h],[2h,4h],[4h,8h], then segments of
-    <= seg_len m up to rho_max.  Returns (nodes, segments) with segments [(a, b, node_idx)]."""
-    edges = [0.0, h, 2 * h, 4 * h, 8 * h]
+    """Piecewise Chebyshev-Lobatto nodes in rho: [0,h],[h,2h],[2h,4h], ... doubling up to seg_len
+    (h = the smallest length scale of the radial functions), then segments of <= seg_len m up to
+    rho_max.  Returns (nodes, segments) with segments [(a, b, node_idx)]."""
+    edges = [0.0, h]
+    while edges[-1] * 2 <= seg_len * (1 + 1e-12):
+        edges.append(edges[-1] * 2)
+    n_geo = len(edges) - 1
     while edges[-1] < rho_max:
         edges.append(min(rho_max, edges[-1] + seg_len) if rho_max - edges[-1] > 0.25 * seg_len
                      else rho_max)
@@ -240,7 +244,7 @@ def radial_nodes(rho_max, h, seg_len=2.0, n_near=16, n_far=20):
         edges.append(rho_max)
     nodes, segs = [], []
     for i, (a, b) in enumerate(zip(edges[:-1], edges[1:])):
-        nn = n_near if i < 4 else n_far
+        nn = n_near if i < n_geo else n_far
         t = np.cos(np.pi * np.arange(nn) / (nn - 1))[::-1]  # -1 .. 1
         x = 0.5 * (a + b) + 0.5 * (b - a) * t
         idx = np.arange(len(nodes), len(nodes) + nn)
@@ -595,7 +599,9 @@ def incident_E_layered_grid(med, x, y, z, src, moments):
         h_min = max(float(dz) + float(ds), 1e-4)
     else:
         h_min = 1.0
-    hseg = min(abs(x[1] - x[0]) if nx > 1 else 0.25, abs(y[1] - y[0]) if ny > 1 else 0.25)
+    # radial segments start at the smallest length scale: the cell size or the source-to-interface
+    # plus cell-to-interface distance (a source next to an interface)
+    hseg = min(abs(x[1] - x[0]) if nx > 1 else 0.25, abs(y[1] - y[0]) if ny > 1 else 0.25, h_min)
     out = np.zeros((len(moments), 3, nz, ny, nx), np.complex128)
     iwm = 1j * med.omega * MU0
     if med.L > 1 or m != 0:

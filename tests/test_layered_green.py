@@ -240,3 +240,32 @@ def test_centroid_on_an_interface_is_rejected():
     med = lg.Medium((1.0, 0.1), (0.0,), 1e5)
     with pytest.raises(AssertionError):
         lg.layered_table(med, (2, 2, 4), (0.25, 0.25, 0.25), (0.0, 0.0, -0.25))
+
+
+def test_grid_incident_field_equals_point_evaluation():
+    """incident_E_layered_grid (the one the layered inputs use: radial functions per depth,
+    interpolated to the (x, y) columns) equals the point evaluation without interpolation, for
+    moments with every component, sources in each layer and next to an interface; and with equal
+    layers it equals the oracle's homogeneous incident field."""
+    med = _med3()
+    x = -1.375 + 0.25 * np.arange(12)
+    y = -0.875 + 0.25 * np.arange(8)
+    z = np.array([-6.125, -4.125, -3.875, 0.125, 2.875, 3.125, 5.375])
+    moms = np.array([[0.3, -0.5, 0.8], [1.0, 0.2, -0.4]])
+    Z, Y, X = np.meshgrid(z, y, x, indexing="ij")
+    P = np.stack([X, Y, Z], -1).reshape(-1, 3)
+    for src in (np.array([0.05, 0.1, 0.4]), np.array([-0.3, 0.2, -5.0]), np.array([0.1, -0.05, 2.98]),
+                np.array([0.2, 0.3, 4.6])):
+        Eg = lg.incident_E_layered_grid(med, x, y, z, src, moms)  # (2, 3, nz, ny, nx)
+        Ep = lg.incident_E_layered(med, P, src, moms, rho_interp=False)  # (2, P, 3)
+        Ep = np.moveaxis(Ep.reshape(2, len(z), len(y), len(x), 3), -1, 1)
+        assert np.abs(Eg - Ep).max() < 1e-9 * np.abs(Ep).max()
+    sig, f = 0.3, 4e5
+    med1 = lg.Medium((sig, sig), (0.3,), f)
+    src = np.array([0.05, 0.1, -0.2])
+    Eg = lg.incident_E_layered_grid(med1, x, y, z * 0.1, src, moms)
+    k0 = physics.wavenumber(sig, f)
+    Z, Y, X = np.meshgrid(z * 0.1, y, x, indexing="ij")
+    for t, m in enumerate(moms):
+        ref = np.moveaxis(physics.incident_E(np.stack([X, Y, Z], -1), src, m, k0, f), -1, 0)
+        assert np.abs(Eg[t] - ref).max() < 1e-10 * np.abs(ref).max()
