@@ -106,3 +106,41 @@ def test_contraction_preconditioner_algebra_and_solution_invariance():
     E = pc.apply_cellwise(P, chi)
     assert np.linalg.norm(E - X) < 1e-9 * np.linalg.norm(X)
     assert np.linalg.norm(E0 - A(E)) / np.linalg.norm(E0) < 1e-11  # the Eq. 9 residual
+
+
+def test_gmres_converges_in_as_many_steps_as_distinct_eigenvalues():
+    """Full GMRES on a normal matrix with d distinct eigenvalues reaches the exact solution in d
+    Arnoldi steps (the minimal polynomial has degree d), and its least-squares residual estimate
+    equals the true residual there -- pins the complex Givens rotations, not only the final answer."""
+    rng = np.random.default_rng(5)
+    lam = np.array([1.0 + 0.5j, 0.7 - 0.2j, 2.0 + 1.0j, 1.3 + 0.0j, 0.9 + 0.9j])
+    n = 40
+    Q, _ = np.linalg.qr(rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n)))
+    D = np.repeat(lam, n // len(lam))
+    M = (Q * D) @ Q.conj().T
+    b = (rng.standard_normal(n) + 1j * rng.standard_normal(n)).reshape(n, 1, 1, 1)
+
+    def A(v):
+        return (M @ v.ravel()).reshape(v.shape)
+
+    x, info = gmres(A, b, tol=1e-12, restart=30)
+    assert info["converged"] and info["iters"] == len(lam)
+    assert abs(info["relres_est"] - info["relres_true"]) < 1e-10
+    # before the last step the estimate is the true least-squares residual of the Krylov space
+    x4, info4 = gmres(A, b, tol=1e-30, restart=30, max_iters=4)
+    assert abs(info4["relres_est"] - info4["relres_true"]) < 1e-10 * max(info4["relres_true"], 1e-300)
+
+
+def test_background_conductivity_is_zero_contrast():
+    """sigma = sigma_b I everywhere is no anomaly (dsigma = sigma - sigma_b I): the operator is
+    the identity bitwise and the solve returns E0 in zero iterations."""
+    n, h, sb, f = (4, 4, 4), (0.25, 0.25, 0.25), 0.7, 2e5
+    k0 = physics.wavenumber(sb, f)
+    sigma = np.broadcast_to(sb * np.eye(3), (4, 4, 4, 3, 3)).copy()
+    ds = physics.contrast(sigma, sb)
+    rng = np.random.default_rng(2)
+    E = rng.standard_normal((3, 4, 4, 4)) + 1j * rng.standard_normal((3, 4, 4, 4))
+    A = op.Operator(n, h, k0, sb, ds)
+    assert np.array_equal(A(E), E)
+    x, info = gmres(A, E, x0=E, tol=1e-12)  # warm start from E0 (Algorithm 1's initial iterate)
+    assert info["iters"] == 0 and np.array_equal(x, E)
