@@ -181,16 +181,12 @@ def _pair_terms(med, k, n, m, cache=None):
 
 
 def _factor(med, u_col, j, kind, z):
-    """e^{-u_j alpha(z)} (Q, nz) and its d/dz sign; alpha = zt - z ('T') or z - zb ('B')."""
+    """e^{-u_j alpha(z)} (Q, nz), alpha = zt - z ('T') or z - zb ('B') (its d/dz factor is +u_j for
+    'T' and -u_j for 'B', applied by the callers)."""
     z = np.asarray(z, np.float64)
-    if kind == "T":
-        a = med.zt(j) - z
-        s = 1.0
-    else:
-        a = z - med.zb(j)
-        s = -1.0
+    a = (med.zt(j) - z) if kind == "T" else (z - med.zb(j))
     assert np.all(a >= 0) and np.all(np.isfinite(a))
-    return np.exp(-u_col[:, None] * a[None, :]), s
+    return np.exp(-u_col[:, None] * a[None, :])
 
 
 def _alpha(med, j, kind, z):
@@ -400,8 +396,8 @@ def dyadic_radial(med, z_obs, z_src, rho, h_min, order=_GL_ORDER):
                         q = int(np.searchsorted(k, _ZETA_CUT / zeta, side="right"))
                         if q == 0:
                             continue
-                        Xo, _ = _factor(med, un[:q], n, a, z_obs[io][bi])
-                        Xs, _ = _factor(med, um[:q], m, b, z_src[js][bj])
+                        Xo = _factor(med, un[:q], n, a, z_obs[io][bi])
+                        Xs = _factor(med, um[:q], m, b, z_src[js][bj])
                         P = (Xo[:, :, None] * Xs[:, None, :]).reshape(q, -1)
                         for f in range(5):
                             V = Wb[f][:q] * cf[f][:q, None]  # (q, R)
@@ -656,8 +652,8 @@ def _mag_radial(med, zu, zs, rho, h_min, m, order=_GL_ORDER):
                 q = int(np.searchsorted(k, _ZETA_CUT / zeta, side="right"))
                 if q == 0:
                     continue
-                Xo, _ = _factor(med, un[:q], n, a, zu[io][bi])
-                Xs, _ = _factor(med, um[:q], m, b, np.array([zs]))
+                Xo = _factor(med, un[:q], n, a, zu[io][bi])
+                Xs = _factor(med, um[:q], m, b, np.array([zs]))
                 X = Xo * Xs  # (q, nb)
                 w1 = (wk * k / (4 * np.pi))[:q, None]
                 w2 = (wk * k ** 2 / (2 * np.pi))[:q, None]
@@ -695,16 +691,16 @@ def incident_H_layered(med, points, src, moments, order=_GL_ORDER):
         # alpha = d_z d_zs G_TE, beta = d_z G_TE, gamma = d_zs G_TE, dlt = G_TE, eps = i w mu0 G_TM
         acc = {key: np.zeros_like(k, dtype=np.complex128) for key in ("al", "be", "ga", "dl", "ep")}
         for c, a, b in terms["TE"]:
-            Xo, _ = _factor(med, un, n, a, np.array([r[2]]))
-            Xs, _ = _factor(med, um, m, b, np.array([src[2]]))
+            Xo = _factor(med, un, n, a, np.array([r[2]]))
+            Xs = _factor(med, um, m, b, np.array([src[2]]))
             X = (Xo * Xs)[:, 0]
             acc["al"] += c * sgn[a] * un * sgn[b] * um * X
             acc["be"] += c * sgn[a] * un * X
             acc["ga"] += c * sgn[b] * um * X
             acc["dl"] += c * X
         for c, a, b in terms["TM"]:
-            Xo, _ = _factor(med, un, n, a, np.array([r[2]]))
-            Xs, _ = _factor(med, um, m, b, np.array([src[2]]))
+            Xo = _factor(med, un, n, a, np.array([r[2]]))
+            Xs = _factor(med, um, m, b, np.array([src[2]]))
             acc["ep"] += iwm * c * (Xo * Xs)[:, 0]
         x = k * rho
         J0, J1, J2 = special.j0(x), special.j1(x), special.jv(2, x)
