@@ -887,10 +887,12 @@ def run_ours(args, cfg, sigma, rank, ws, local):
             key = {"full": "full_gmres", "jacobi": "jacobi_a", "gauss_seidel": "gs_a" if adaptive else "gs_f",
                    "fgmres_jacobi": "jacobi_fgmres", "fgmres_gauss_seidel": "gs_fgmres"}[scheme] + \
                 ("_cie" if pc else "")
-            dd[key] = {"s_per_position": float(np.median(times)), "sweeps": st["sweeps"],
+            status = ie.STATUS.get(st["status"], st["status"])
+            # a scheme that did not converge has no s/position ("n/a"); its measured time is kept
+            dd[key] = {"s_per_position": float(np.median(times)) if status == "IE_OK" else None,
+                       "s_measured": float(np.median(times)), "sweeps": st["sweeps"],
                        "gmres_iters": st["total_inner_iters"], "full_applies": st["full_applies"],
-                       "sub_applies": st["sub_applies"], "e_final": st["e_final"],
-                       "status": ie.STATUS.get(st["status"], st["status"])}
+                       "sub_applies": st["sub_applies"], "e_final": st["e_final"], "status": status}
     return dict(value=value, per_step=per_step, launches=launches, clk=clk.summary(), peak=peak,
                 peak_src=peak_src, dom=dom, achieved=achieved, kernels=kernels, e2e=e2e, dd=dd, bm=bm, cufft=cufft,
                 layered=layered, sweep=sweep, window=window, op_c4h=op_c4h,
