@@ -163,6 +163,32 @@ def test_fullsize_c4mid_dd_agrees_with_full_and_oracle_residual():
         r = E0[s][:, [c[2] for c in cells], [c[1] for c in cells], [c[0] for c in cells]].T \
             - lay.direct_rows_layered(T, ds, Ef[s], cells)
         assert np.abs(r).max() < 1e-7 * np.abs(E0[s]).max()
+    # the receiver couplings (reciprocity form, R17) of the GPU field against the oracle's sum
+    for s in range(3):
+        ref = np.array([lay.receiver_coupling(Ef[s], ds, e0rx[d], h0[s, d], cfg.h ** 3, med.omega)
+                        for d in range(len(e0rx))])
+        assert rel(Hf[s], ref) < 1e-12
+
+
+def test_fullsize_literal_c4_solve_oracle_residual():
+    """Literal c4 (the resistive slab through the 1 S/m shoulders, R23), station 31, 400 kHz: full
+    GMRES + contraction IE to 1e-6 converges (thousands of iterations), and the oracle's direct
+    layered sum gives an Eq. 9 residual at that level at sampled cells, two of them in the slab."""
+    import torch
+    import paper_2306_17537_b200 as ie
+    cfg, med, T, sig, ds, E0 = _setup("c4")
+    nx, ny, nz = cfg.n
+    ctx = _ctx(cfg, T, sig, 3, [])
+    ie.ie_set_incident(ctx, torch.from_numpy(E0).cuda())
+    e = torch.empty(E0.shape, dtype=torch.complex128, device="cuda")
+    st = ie.ie_solve_dd(ctx, e, "full", outer_tol=1e-6, restart=30, max_iters=8000, precond=1)
+    assert st["e_final"] <= 1e-6
+    E = e.cpu().numpy()
+    cells = [(nx // 2, ny // 2, nz // 2), (64, 64, 24), (10, 100, 50), (120, 5, 12)]
+    for s in range(3):
+        r = E0[s][:, [c[2] for c in cells], [c[1] for c in cells], [c[0] for c in cells]].T \
+            - lay.direct_rows_layered(T, ds, E[s], cells)
+        assert np.abs(r).max() < 1e-4 * np.abs(E0[s]).max()
 
 
 @pytest.mark.slow
