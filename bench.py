@@ -20,7 +20,6 @@ import argparse
 import json
 import math
 import os
-import subprocess
 import sys
 import threading
 import time

@@ -8,7 +8,7 @@ import pytest
 
 from ie_workloads import make_config
 from oracle import physics, operator as op
-from gpu_helpers import gpu_ctx, rel
+from gpu_helpers import gpu_ctx
 
 pytestmark = pytest.mark.gpu
 

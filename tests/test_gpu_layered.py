@@ -7,7 +7,7 @@ import numpy as np
 import pytest
 
 from ie_workloads import Config
-from oracle import physics, operator as op, layered as lay, dd
+from oracle import physics, layered as lay
 from gpu_helpers import rel
 
 pytestmark = pytest.mark.gpu

@@ -7,7 +7,6 @@ import numpy as np
 import pytest
 
 from oracle import physics, operator as op, layered as lay, dd
-from oracle.gmres import gmres
 
 
 def _hom(n, h=0.25, sigma_b=0.7, f=2e5):

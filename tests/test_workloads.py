@@ -7,7 +7,7 @@ import os
 import numpy as np
 import pytest
 
-from ie_workloads import make_config, vti_tensor, haar_rotation, box_grid, CONFIG_NAMES
+from ie_workloads import make_config, vti_tensor, haar_rotation, box_grid
 from ie_workloads.configs import c4_stations
 
 GOLD = os.path.join(os.path.dirname(__file__), "golden")

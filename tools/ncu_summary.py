@@ -1,10 +1,8 @@
 """Summarise an ncu --set full report: headline metrics plus stall samples per source line."""
 import csv
 import io
-import re
 import subprocess
 import sys
-from collections import Counter
 
 rep = sys.argv[1]
 src_file = sys.argv[2] if len(sys.argv) > 2 else None
