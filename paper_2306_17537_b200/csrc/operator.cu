@@ -439,7 +439,7 @@ __global__ void __launch_bounds__(128, 2) k_zconv16(const __grid_constant__ Appl
 // plane iz = min(kz, L - kz) falls in it, for every u), and the inverse starts from registers.
 // Stage twiddles w^(r j) = w^(4a j) w^(b j) (r = 4a + b) from two loaded powers.  Threads of
 // mirror-partner pencil positions (t, T - t) share a warp.
-template <int L>
+template <int L, bool kHoistTw = true>
 __global__ void __launch_bounds__(128, 3) k_zconv_tm(const __grid_constant__ ApplyParams p) {
   constexpr int NZ = L / 2, T = L / 16, W = 2048 / L, R1 = L / 16, U = 16 / R1;
   constexpr int CH = NZ / 4, GR = CH + 1;  // Green chunk: planes [CH k, CH k + CH]
@@ -517,6 +517,24 @@ __global__ void __launch_bounds__(128, 3) k_zconv_tm(const __grid_constant__ App
       v[r] = CONJ ? cmulc(v[r], w) : cmul(v[r], w);
     }
   };
+  // L = 256 (U = 1, j = t): the 15 stage twiddles w^(r t) are the same for the three forward and
+  // (conjugated) the three inverse transforms -- generated once per direction and kept in registers
+  constexpr bool HOIST = (L == 256) && kHoistTw;
+  double2 twr[HOIST ? 16 : 1];
+  auto make_tw = [&]() {
+    if constexpr (HOIST) {
+      const double2 b1 = twl[t], a1 = twl[4 * t];
+      const double2 b2 = cmul(b1, b1), b3 = cmul(b2, b1);
+      const double2 a2 = cmul(a1, a1), a3 = cmul(a2, a1);
+      const double2 bb[4] = {make_double2(1.0, 0.0), b1, b2, b3};
+      const double2 aa[4] = {make_double2(1.0, 0.0), a1, a2, a3};
+#pragma unroll
+      for (int r = 1; r < 16; ++r) {
+        const int a = r >> 2, b = r & 3;
+        twr[r] = (a == 0) ? bb[b] : (b == 0 ? aa[a] : cmul(aa[a], bb[b]));
+      }
+    }
+  };
   auto forward = [&](int l, double2(&v)[16], bool hook) {
 #pragma unroll
     for (int r = 0; r < 8; ++r) v[r] = sm[(l * NZ + t + r * T) * W + c];  // z = t + r T < nz
@@ -537,7 +555,12 @@ __global__ void __launch_bounds__(128, 3) k_zconv_tm(const __grid_constant__ App
       const double2* hi = sm + (3 * NZ + j) * W + c - (long long)NZ * W;
 #pragma unroll
       for (int r = 0; r < R1; ++r) v[u * R1 + r] = (r < R1 / 2 ? lo : hi)[16 * r * W];
-      twiddle(&v[u * R1], R1, j, std::false_type{});
+      if constexpr (HOIST) {
+#pragma unroll
+        for (int r = 1; r < 16; ++r) v[r] = cmul(v[r], twr[r]);
+      } else {
+        twiddle(&v[u * R1], R1, j, std::false_type{});
+      }
       dftR<R1, -1>(&v[u * R1]);  // v[u R1 + r] = spectrum at kz = j + 16 r
     }
   };
@@ -546,6 +569,7 @@ __global__ void __launch_bounds__(128, 3) k_zconv_tm(const __grid_constant__ App
   auto chunk_of = [](int r) { return r < R1 / 2 ? (16 * r) / CH : (16 * (R1 - 1 - r)) / CH; };
 
   double2 v[16];
+  make_tw();
 #pragma unroll 1
   for (int l = 0; l < 2; ++l) {
     forward(l, v, false);
@@ -604,12 +628,18 @@ __global__ void __launch_bounds__(128, 3) k_zconv_tm(const __grid_constant__ App
     __syncthreads();
 #pragma unroll
     for (int r = 0; r < 16; ++r) v[r] = B[(t + r * T) * W + c];
-    twiddle(v, 16, t, std::true_type{});  // exp(+2 pi i r t / L)
+    if constexpr (HOIST) {
+#pragma unroll
+      for (int r = 1; r < 16; ++r) v[r] = cmulc(v[r], twr[r]);  // exp(+2 pi i r t / L)
+    } else {
+      twiddle(v, 16, t, std::true_type{});  // exp(+2 pi i r t / L)
+    }
     dft16<+1, false, true>(v);
     double2* dst = tile + l * cs + c;
 #pragma unroll
     for (int r = 0; r < 8; ++r) dst[(long long)(t + r * T) * zs] = v[r];  // z = t + r T < nz
   };
+  make_tw();
   inverse(2, v, sm);
 #pragma unroll 1
   for (int l = 0; l < 2; ++l) {
@@ -1179,14 +1209,23 @@ static cudaError_t go_zconv16_w(const ApplyParams& p, cudaStream_t s) {
   k_zconv16<L, W><<<dim3(p.n_items * (p.x2w / W), 2 * p.ny), W * (L / 16), smem, s>>>(p);
   return cudaGetLastError();
 }
-template <int L>
-static cudaError_t go_zconv_tm(const ApplyParams& p, cudaStream_t s) {
+template <int L, bool HT>
+static cudaError_t go_zconv_tm_h(const ApplyParams& p, cudaStream_t s) {
   constexpr int W = 2048 / L;
   const size_t smem = (size_t)(4 * (L / 2) * W + L + 1) * sizeof(double2);
-  cudaError_t e = prep((const void*)k_zconv_tm<L>, smem);
+  cudaError_t e = prep((const void*)k_zconv_tm<L, HT>, smem);
   if (e) return e;
-  k_zconv_tm<L><<<dim3(p.n_items * (p.x2w / W), 2 * p.ny), 128, smem, s>>>(p);
+  k_zconv_tm<L, HT><<<dim3(p.n_items * (p.x2w / W), 2 * p.ny), 128, smem, s>>>(p);
   return cudaGetLastError();
+}
+template <int L>
+static cudaError_t go_zconv_tm(const ApplyParams& p, cudaStream_t s) {
+  // IE_KC_HOIST=0: per-transform stage twiddles (L = 256) instead of once per direction
+  static const int hoist = [] {
+    const char* v = getenv("IE_KC_HOIST");
+    return v ? atoi(v) : 1;
+  }();
+  return hoist ? go_zconv_tm_h<L, true>(p, s) : go_zconv_tm_h<L, false>(p, s);
 }
 static cudaError_t go_zconv16(const ApplyParams& p, cudaStream_t s, int W) {
   const int L = 2 * p.nz;
