@@ -439,7 +439,37 @@ __global__ void __launch_bounds__(128, 2) k_zconv16(const __grid_constant__ Appl
 // plane iz = min(kz, L - kz) falls in it, for every u), and the inverse starts from registers.
 // Stage twiddles w^(r j) = w^(4a j) w^(b j) (r = 4a + b) from two loaded powers.  Threads of
 // mirror-partner pencil positions (t, T - t) share a warp.
-template <int L, bool kHoistTw = true>
+// the e-th stage-2 index r (ascending) whose Green octant plane falls in chunk k of the TMEM
+// z-pass (chunk_of below); R1 = L/16 radix, CH = L/8 planes per chunk
+template <int L>
+__host__ __device__ constexpr int chunk_r(int k, int e) {
+  constexpr int R1 = L / 16, CH = L / 8;
+  int n = 0;
+  for (int r = 0; r < R1; ++r) {
+    const int ck = r < R1 / 2 ? (16 * r) / CH : (16 * (R1 - 1 - r)) / CH;
+    if (ck == k) {
+      if (n == e) return r;
+      ++n;
+    }
+  }
+  return -1;
+}
+static_assert(chunk_r<256>(0, 3) == 15 && chunk_r<256>(3, 0) == 6 && chunk_r<128>(0, 1) == 7 && chunk_r<128>(2, 0) == 2,
+              "chunk slot enumeration");
+
+// dft16 / dftR with the inner twiddles folded into the butterflies (FMA = true) or not
+template <bool FMA, int DIR, bool HI = false, bool HO = false>
+__device__ __forceinline__ void dft16k(double2* v) {
+  if constexpr (FMA) dft16f<DIR, HI, HO>(v);
+  else dft16<DIR, HI, HO>(v);
+}
+template <bool FMA, int R, int DIR>
+__device__ __forceinline__ void dftRk(double2* v) {
+  if constexpr (R == 16) dft16k<FMA, DIR>(v);
+  else dftR<R, DIR>(v);
+}
+
+template <int L, bool kHoistTw = true, bool kPairMul = true, bool kFmaDft = true>
 __global__ void __launch_bounds__(128, 3) k_zconv_tm(const __grid_constant__ ApplyParams p) {
   constexpr int NZ = L / 2, T = L / 16, W = 2048 / L, R1 = L / 16, U = 16 / R1;
   constexpr int CH = NZ / 4, GR = CH + 1;  // Green chunk: planes [CH k, CH k + CH]
@@ -480,7 +510,9 @@ __global__ void __launch_bounds__(128, 3) k_zconv_tm(const __grid_constant__ App
         if (z >= z0 && z < z1) cp_async16(d, tile + l * cs + z * zs + c);
         else *d = czero();
       }
-    for (int m = threadIdx.x; m < L; m += blockDim.x) cp_async16(&twl[m], &p.pw_z[m]);
+    {
+      for (int m = threadIdx.x; m < L; m += blockDim.x) cp_async16(&twl[m], &p.pw_z[m]);
+    }
     cp_async_wait_all();  // (no L2 prefetch of the Green rows: the chunk copies run a pass ahead)
     tmem_fence_before();
     __syncthreads();
@@ -538,7 +570,7 @@ __global__ void __launch_bounds__(128, 3) k_zconv_tm(const __grid_constant__ App
   auto forward = [&](int l, double2(&v)[16], bool hook) {
 #pragma unroll
     for (int r = 0; r < 8; ++r) v[r] = sm[(l * NZ + t + r * T) * W + c];  // z = t + r T < nz
-    dft16<-1, true>(v);
+    dft16k<kFmaDft, -1, true>(v);
     __syncthreads();  // every input row of component l read before the exchange overwrites it
     if (hook) g_chunk(0, RA);  // blocks 0-1 are free once component 1 is done
     {  // rows t*16 .. t*16+15 lie on one side of NZ (a multiple of 16): one select per pass
@@ -561,7 +593,7 @@ __global__ void __launch_bounds__(128, 3) k_zconv_tm(const __grid_constant__ App
       } else {
         twiddle(&v[u * R1], R1, j, std::false_type{});
       }
-      dftR<R1, -1>(&v[u * R1]);  // v[u R1 + r] = spectrum at kz = j + 16 r
+      dftRk<kFmaDft, R1, -1>(&v[u * R1]);  // v[u R1 + r] = spectrum at kz = j + 16 r
     }
   };
   const unsigned fx = kx > nx ? 0x80000000u : 0u, fy = ky > ny ? 0x80000000u : 0u;
@@ -588,6 +620,46 @@ __global__ void __launch_bounds__(128, 3) k_zconv_tm(const __grid_constant__ App
     if (k == 1) g_chunk(2, RA);
     if (k == 2) g_chunk(3, RB);
     const double2* R = (k & 1) ? RB : RA;
+    if constexpr (kPairMul) {
+      // the chunk's four slots in two pairs: both slots' Green loads and TMEM loads are issued
+      // before one wait, so their latencies overlap
+#pragma unroll
+      for (int pr = 0; pr < 2; ++pr) {
+        double2 G[2][6];
+        uint32_t raw[2][8];
+        int sl[2], jj[2];
+        unsigned fzz[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int e = 2 * pr + h;
+          const int r = U == 1 ? chunk_r<L>(k, e) : chunk_r<L>(k, e >> 1), u = U == 1 ? 0 : (e & 1);
+          const int s = u * R1 + r, j = t + u * T;
+          sl[h] = s;
+          jj[h] = j;
+          const double2* gr = r < R1 / 2 ? R + (j + 16 * r - CH * k) * W + c : R + (L - j - 16 * r - CH * k) * W + c;
+#pragma unroll
+          for (int q6 = 0; q6 < 6; ++q6) G[h][q6] = gr[q6 * GR * W];
+          fzz[h] = (r < R1 / 2 || (r == R1 / 2 && j == 0)) ? 0u : 0x80000000u;
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          tmem_ld4_raw(taddr + 4 * sl[h], raw[h]);
+          tmem_ld4_raw(taddr + 64 + 4 * sl[h], raw[h] + 4);
+        }
+        tmem_wait_ld16(&raw[0][0]);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const double2 gxy = flip_if(G[h][3], fx ^ fy), gxz = flip_if(G[h][4], fx ^ fzz[h]),
+                        gyz = flip_if(G[h][5], fy ^ fzz[h]);
+          const double2 j0 = raw_to_z(raw[h]), j1 = raw_to_z(raw[h] + 4), j2 = v[sl[h]];
+          tmem_st1(taddr + 4 * sl[h], cdot3(G[h][0], j0, gxy, j1, gxz, j2));
+          tmem_st1(taddr + 64 + 4 * sl[h], cdot3(gxy, j0, G[h][1], j1, gyz, j2));
+          v[sl[h]] = cdot3(gxz, j0, gyz, j1, G[h][2], j2);
+        }
+        (void)jj;
+      }
+      continue;
+    }
 #pragma unroll
     for (int r = 0; r < R1; ++r) {
       if (chunk_of(r) != k) continue;
@@ -618,7 +690,7 @@ __global__ void __launch_bounds__(128, 3) k_zconv_tm(const __grid_constant__ App
   // inverse z-FFT from registers: radix R1 per j, exchange, twiddle + radix 16, crop, store
   auto inverse = [&](int l, double2(&v)[16], double2* B) {
 #pragma unroll
-    for (int u = 0; u < U; ++u) dftR<R1, +1>(&v[u * R1]);
+    for (int u = 0; u < U; ++u) dftRk<kFmaDft, R1, +1>(&v[u * R1]);
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int j = t + u * T;
@@ -634,7 +706,7 @@ __global__ void __launch_bounds__(128, 3) k_zconv_tm(const __grid_constant__ App
     } else {
       twiddle(v, 16, t, std::true_type{});  // exp(+2 pi i r t / L)
     }
-    dft16<+1, false, true>(v);
+    dft16k<kFmaDft, +1, false, true>(v);
     double2* dst = tile + l * cs + c;
 #pragma unroll
     for (int r = 0; r < 8; ++r) dst[(long long)(t + r * T) * zs] = v[r];  // z = t + r T < nz
@@ -1072,6 +1144,7 @@ static void fill_tw(std::vector<double2>& out, bool rev) {
 const double2* Twiddles::get(int L, int rev) const { return dev + off[ilog2i(L)][rev ? 1 : 0]; }
 const double2* Twiddles::powers(int L) const { return dev + pw[ilog2i(L)]; }
 
+
 ie_status build_twiddles(ie_ctx* c) {
   std::vector<double2> h;
   h.push_back(make_double2(1, 0));  // keep offsets of 1-stage plans valid
@@ -1209,23 +1282,35 @@ static cudaError_t go_zconv16_w(const ApplyParams& p, cudaStream_t s) {
   k_zconv16<L, W><<<dim3(p.n_items * (p.x2w / W), 2 * p.ny), W * (L / 16), smem, s>>>(p);
   return cudaGetLastError();
 }
-template <int L, bool HT>
+template <int L, bool HT, bool PM, bool FM>
 static cudaError_t go_zconv_tm_h(const ApplyParams& p, cudaStream_t s) {
   constexpr int W = 2048 / L;
   const size_t smem = (size_t)(4 * (L / 2) * W + L + 1) * sizeof(double2);
-  cudaError_t e = prep((const void*)k_zconv_tm<L, HT>, smem);
+  cudaError_t e = prep((const void*)k_zconv_tm<L, HT, PM, FM>, smem);
   if (e) return e;
-  k_zconv_tm<L, HT><<<dim3(p.n_items * (p.x2w / W), 2 * p.ny), 128, smem, s>>>(p);
+  k_zconv_tm<L, HT, PM, FM><<<dim3(p.n_items * (p.x2w / W), 2 * p.ny), 128, smem, s>>>(p);
   return cudaGetLastError();
 }
 template <int L>
 static cudaError_t go_zconv_tm(const ApplyParams& p, cudaStream_t s) {
-  // IE_KC_HOIST=0: per-transform stage twiddles (L = 256) instead of once per direction
-  static const int hoist = [] {
-    const char* v = getenv("IE_KC_HOIST");
-    return v ? atoi(v) : 1;
+  // A/B switches: IE_KC_HOIST=0: per-transform stage twiddles (L = 256)
+  // instead of once per direction; IE_KC_PAIR (default on for L = 128 only): the spectral
+  // multiply in slot pairs (one TMEM wait per pair); IE_KC_FMA=0: dft16 with separate
+  // inner-twiddle products
+  static const int sw = [] {
+    auto get = [](const char* n, bool dflt) {
+      const char* v = getenv(n);
+      return v ? atoi(v) != 0 : dflt;
+    };
+    return (get("IE_KC_HOIST", true) ? 4 : 0) | (get("IE_KC_PAIR", L == 128) ? 2 : 0) | (get("IE_KC_FMA", true) ? 1 : 0);
   }();
-  return hoist ? go_zconv_tm_h<L, true>(p, s) : go_zconv_tm_h<L, false>(p, s);
+  switch (sw) {
+    case 7: return go_zconv_tm_h<L, true, true, true>(p, s);
+    case 6: return go_zconv_tm_h<L, true, true, false>(p, s);
+    case 5: return go_zconv_tm_h<L, true, false, true>(p, s);
+    case 3: return go_zconv_tm_h<L, false, true, true>(p, s);
+    default: return go_zconv_tm_h<L, false, false, false>(p, s);
+  }
 }
 static cudaError_t go_zconv16(const ApplyParams& p, cudaStream_t s, int W) {
   const int L = 2 * p.nz;

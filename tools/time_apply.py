@@ -14,6 +14,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="c5")
 ap.add_argument("--steps", type=int, default=20)
 ap.add_argument("--nrhs", type=int, default=1)
+ap.add_argument("--kernels", action="store_true", help="also print per-kernel ms (CUDA-event marks)")
 a = ap.parse_args()
 cfg = make_config(a.config)
 ctx = ie.ie_create(cfg.n, cfg.hvec, cfg.origin, cfg.sigma_b, cfg.freq)
@@ -36,3 +37,11 @@ torch.cuda.synchronize()
 t2 = time.perf_counter()
 print(f"{a.config} ms/apply {e0.elapsed_time(e1) / a.steps:.4f} "
       f"host-enqueue ms/apply {(t1 - t0) * 1e3 / a.steps:.4f} wall ms/apply {(t2 - t0) * 1e3 / a.steps:.4f}")
+if a.kernels:
+    ie.ie_profile(ctx, True)
+    for _ in range(a.steps):
+        ie.ie_apply_operator(ctx, x, y)
+    torch.cuda.synchronize()
+    prof = ie.ie_profile_read(ctx)
+    ie.ie_profile(ctx, False)
+    print(a.config, " ".join(f"{k.split()[0]} {v[0] / max(v[1], 1):.4f}" for k, v in prof.items() if v[1]))
