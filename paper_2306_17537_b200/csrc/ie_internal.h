@@ -60,6 +60,7 @@ struct ApplyParams {
   const double2* pw_z;   // exp(-2 pi i m / 2nz), m < 2nz (radix-16 z-pass)
   const double2* mhat;   // layered background: packed z-z' spectra (layered.cu), else null
   int n_items;
+  int rev;  // K-B / K-E: CTAs walk their tiles in reverse launch order (set per launch, operator.cu)
   ApplyItem items[kMaxItems];
 };
 

@@ -99,11 +99,22 @@ __global__ void __launch_bounds__(512) k_yfwd(const __grid_constant__ ApplyParam
   extern __shared__ double2 sm[];
   const int W = blockDim.x / T;
   const int c = threadIdx.x % W, t = threadIdx.x / W;
-  const int item = blockIdx.z / 3, q = blockIdx.z % 3;
+  // rev: the launch order runs from the last plane of every component down to the first, so
+  // the first CTAs read the rows K-A wrote last (still in L2)
+  int bx = blockIdx.x, by = blockIdx.y, bz = blockIdx.z;
+  if (p.rev) {
+    const int id = (int)(gridDim.x * gridDim.y * gridDim.z) - 1 -
+                   (int)(blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z));
+    bx = id % gridDim.x;
+    const int rest = id / gridDim.x;
+    bz = rest % gridDim.z;
+    by = rest / gridDim.z;
+  }
+  const int item = bz / 3, q = bz % 3;
   const ApplyItem& it = p.items[item];
   const int Lx = 2 * p.nx, Xw = p.x2w;  // X2 row width: 2nx, or the slab width (slab pipeline)
-  const int kx = p.k0x + blockIdx.x * W + c;
-  const int z = it.sz0 + blockIdx.y;
+  const int kx = p.k0x + bx * W + c;
+  const int z = it.sz0 + by;
   const double2* src = p.X1 + (((long long)item * 3 + q) * p.nz + z) * p.ny * Lx + kx;
   double2 v[1][V];
 #pragma unroll
@@ -763,12 +774,19 @@ __global__ void __launch_bounds__(128) k_xinv(const __grid_constant__ ApplyParam
   using P = FftPlan<L>;
   constexpr int T = P::T, V = P::V, R0 = P::radix(0, false), RL = P::radix(P::NST - 1, false);
   extern __shared__ double2 sm[];
-  const int item = blockIdx.y / 3, l = blockIdx.y % 3;
+  // rev: reverse launch order (the first CTAs read the planes K-D wrote last, still in L2)
+  int bx = blockIdx.x, by = blockIdx.y;
+  if (p.rev) {
+    const int id = (int)(gridDim.x * gridDim.y) - 1 - (int)(blockIdx.x + gridDim.x * blockIdx.y);
+    bx = id % gridDim.x;
+    by = id / gridDim.x;
+  }
+  const int item = by / 3, l = by % 3;
   const ApplyItem& it = p.items[item];
   const int rows_cta = blockDim.x / T;
   const int lr = threadIdx.x / T, t = threadIdx.x % T;
   const int nx = p.nx, ny = p.ny, nz = p.nz;
-  const int row = blockIdx.x * rows_cta + lr;
+  const int row = bx * rows_cta + lr;
   const bool valid = row < ny * nz;
   const int yy = valid ? row % ny : 0, zz = valid ? row / ny : 0;
   const long long N = (long long)nx * ny * nz;
@@ -1208,6 +1226,16 @@ static cudaError_t prep(const void* kernel, size_t smem) {
   return e;
 }
 
+// IE_REV=0: K-B and K-E walk their tiles in launch order instead of reverse order (reverse: the
+// first CTAs read what the previous pass wrote last, while it is still in L2)
+static int rev_order() {
+  static const int r = [] {
+    const char* v = getenv("IE_REV");
+    return v ? atoi(v) : 1;
+  }();
+  return r;
+}
+
 // x-passes: rows_cta rows of 3 lines; y-passes: W columns; z-pass: W columns of 3 lines
 static int rows_per_cta(int T) { return T >= 128 ? 1 : 128 / T; }
 static int y_width(int T, int Lx) {
@@ -1254,7 +1282,9 @@ static cudaError_t go_yfwd(const ApplyParams& p, cudaStream_t s, int max_planes)
   const size_t smem = (size_t)padded(L * W) * sizeof(double2);
   cudaError_t e = prep((const void*)k_yfwd<L>, smem);
   if (e) return e;
-  k_yfwd<L><<<dim3(p.x2w / W, max_planes, 3 * p.n_items), W * T, smem, s>>>(p);
+  ApplyParams q = p;
+  q.rev = rev_order();
+  k_yfwd<L><<<dim3(p.x2w / W, max_planes, 3 * p.n_items), W * T, smem, s>>>(q);
   return cudaGetLastError();
 }
 template <int L>
@@ -1356,7 +1386,9 @@ static cudaError_t go_xinv_p(const ApplyParams& p, cudaStream_t s) {
   const size_t smem = (size_t)rows * padded(L) * sizeof(double2);
   cudaError_t e = prep((const void*)k_xinv<L, PRE>, smem);
   if (e) return e;
-  k_xinv<L, PRE><<<dim3((p.ny * p.nz + rows - 1) / rows, 3 * p.n_items), rows * T, smem, s>>>(p);
+  ApplyParams q = p;
+  q.rev = rev_order();
+  k_xinv<L, PRE><<<dim3((p.ny * p.nz + rows - 1) / rows, 3 * p.n_items), rows * T, smem, s>>>(q);
   return cudaGetLastError();
 }
 template <int L>
