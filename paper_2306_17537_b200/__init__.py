@@ -15,7 +15,7 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libie_b200.so")
+LIB_PATH = os.environ.get("IE_LIB_PATH") or os.path.join(HERE, "libie_b200.so")  # IE_LIB_PATH: A/B of an alternative build (tools/gpu_ab_lib.sh)
 
 IE_OK = 0
 STATUS = {0: "IE_OK", 1: "IE_ERR_INVALID_ARGUMENT", 2: "IE_ERR_OUT_OF_MEMORY", 3: "IE_ERR_CUDA",
