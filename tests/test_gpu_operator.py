@@ -157,18 +157,23 @@ def test_config_operator_matches_oracle_fft(name):
         assert rel(yh[r], A(E0[r])) < TOL
 
 
-@pytest.mark.parametrize("env", ["IE_KC_VARIANT=0", "IE_KC128_VARIANT=0"])
+@pytest.mark.parametrize("env", ["IE_KC_VARIANT=0", "IE_KC128_VARIANT=0",
+                                 "IE_KC_HOIST=0,IE_KC_PAIR=0,IE_KC_FMA=0", "IE_KC_PAIR=1", "IE_KC_FMA=0,IE_KC_PAIR=0",
+                                 "IE_REV=0"])
 def test_zpass_variants_match_oracle(env):
-    """The non-default (shared-memory-parked) z-pass kernels, IE_KC_VARIANT=0 for L = 256 and
-    IE_KC128_VARIANT=0 for L = 128 (read once per process, hence the subprocess), pass the same
-    operator parity as the default TMEM kernels."""
+    """The non-default z-pass kernels and launch orders pass the same operator parity as the
+    defaults (switches are read once per process, hence the subprocess): the shared-memory-parked
+    z-passes (IE_KC_VARIANT=0 for L = 256, IE_KC128_VARIANT=0 for L = 128), the TMEM z-pass
+    without the round-2 instruction cuts (per-transform twiddles, per-slot multiply, plain
+    radix 16), with the paired multiply at L = 256 and without the FMA-shaped radix 16, and the
+    K-B / K-E tiles in launch order (IE_REV=0)."""
     import os
     import subprocess
     import sys
-    k, v = env.split("=")
+    extra = dict(kv.split("=") for kv in env.split(","))
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider",
                         os.path.abspath(__file__) + "::test_apply_operator_matches_oracle"],
-                       env=dict(os.environ, **{k: v}), capture_output=True, text=True, timeout=900)
+                       env=dict(os.environ, **extra), capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
 
 
