@@ -159,14 +159,15 @@ def test_config_operator_matches_oracle_fft(name):
 
 @pytest.mark.parametrize("env", ["IE_KC_VARIANT=0", "IE_KC128_VARIANT=0",
                                  "IE_KC_HOIST=0,IE_KC_PAIR=0,IE_KC_FMA=0", "IE_KC_PAIR=1", "IE_KC_FMA=0,IE_KC_PAIR=0",
-                                 "IE_REV=0"])
+                                 "IE_REV=0", "IE_PDL=0", "IE_PDL=1"])
 def test_zpass_variants_match_oracle(env):
     """The non-default z-pass kernels and launch orders pass the same operator parity as the
     defaults (switches are read once per process, hence the subprocess): the shared-memory-parked
     z-passes (IE_KC_VARIANT=0 for L = 256, IE_KC128_VARIANT=0 for L = 128), the TMEM z-pass
     without the round-2 instruction cuts (per-transform twiddles, per-slot multiply, plain
     radix 16), with the paired multiply at L = 256 and without the FMA-shaped radix 16, and the
-    K-B / K-E tiles in launch order (IE_REV=0)."""
+    K-B / K-E tiles in launch order (IE_REV=0), and the passes without / always with programmatic
+    dependent launch (IE_PDL=0 / 1; the default uses it on grids of <= 2^18 cells)."""
     import os
     import subprocess
     import sys
