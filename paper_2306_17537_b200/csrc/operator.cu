@@ -28,13 +28,26 @@ namespace ie {
 
 __device__ __forceinline__ double2 ld2(const double2* p) { return __ldg(p); }
 
-// Programmatic dependent launch (IE_PDL=1): a pass launched with the PDL attribute may start
-// while the previous pass drains; every global access of the pass comes after pdl_wait(), which
-// returns once the previous grid has completed and its writes are visible (a no-op without the
-// attribute).  pdl_trigger() lets the next pass's CTAs be scheduled once all of this pass's CTAs
-// are running (they then wait in pdl_wait on freed SMs instead of after the last CTA exits).
+#ifndef IE_PDL_LATE
+#define IE_PDL_LATE 1  // 0: trigger the dependent pass at CTA start instead of CTA exit (A/B build)
+#endif
+// Programmatic dependent launch (launch_pass): a pass launched with the PDL attribute may be
+// scheduled before the previous pass has finished; every global access of the pass comes after
+// pdl_wait(), which returns once the previous grid has completed and its writes are visible (a
+// no-op without the attribute).  The trigger that lets the next pass's CTAs be scheduled is issued
+// as each CTA finishes (pdl_trigger_late), so they take the SMs the exiting CTAs free.
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
-__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+#if !IE_PDL_LATE
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
+}
+__device__ __forceinline__ void pdl_trigger_late() {
+#if IE_PDL_LATE
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
+}
+
 
 // =====================================================================  K-A
 template <int L>
@@ -99,6 +112,7 @@ __global__ void __launch_bounds__(128, 5) k_xfwd(const __grid_constant__ ApplyPa
         for (int r = 0; r < RL; ++r) out[t + u * T + r * (L / RL)] = v[0][u * RL + r];
     }
   }
+  pdl_trigger_late();
 }
 
 // =====================================================================  K-B
@@ -143,6 +157,7 @@ __global__ void __launch_bounds__(512) k_yfwd(const __grid_constant__ ApplyParam
   for (int u = 0; u < V / RL; ++u)
 #pragma unroll
     for (int r = 0; r < RL; ++r) dst[(long long)(t + u * T + r * (L / RL)) * Xw] = v[0][u * RL + r];
+  pdl_trigger_late();
 }
 
 // =====================================================================  K-C
@@ -750,6 +765,7 @@ __global__ void __launch_bounds__(128, 3) k_zconv_tm(const __grid_constant__ App
     tmem_fence_after();
     tmem_dealloc(*tslot, kCols);
   }
+  pdl_trigger_late();
 }
 
 // =====================================================================  K-D
@@ -779,6 +795,7 @@ __global__ void __launch_bounds__(512, 2) k_yinv(const __grid_constant__ ApplyPa
   for (int u = 0; u < V / RL; ++u)
 #pragma unroll
     for (int r = 0; r < RL / 2; ++r) dst[(long long)(t + u * T + r * (L / RL)) * Lx] = v[0][u * RL + r];
+  pdl_trigger_late();
 }
 
 // =====================================================================  K-E
@@ -850,6 +867,7 @@ __global__ void __launch_bounds__(128) k_xinv(const __grid_constant__ ApplyParam
       if (p.accumulate) o = cadd(o, yrow[x]);
       yrow[x] = o;
     }
+  pdl_trigger_late();
 }
 
 // =====================================================================  K-DE (fused)
@@ -1254,17 +1272,18 @@ static int rev_order() {
   return r;
 }
 
-// Launch one operator pass, with the programmatic-dependent-launch attribute on small grids
-// (N <= 2^18 cells per launch, where the passes are launch-latency bound: c2mod apply 0.0353 ->
-// 0.0323 ms); on large grids it measured slower (c4h 0.342 -> 0.369 ms) and neutral on c5.
-// IE_PDL=0 / 1 forces it off / on.
-static bool use_pdl(const ApplyParams& p) {
+// Launch one operator pass with the programmatic-dependent-launch attribute: the next pass's CTAs
+// are scheduled as this pass's CTAs exit (pdl_trigger_late) and wait for its completion in
+// pdl_wait, so the pass boundary costs no launch gap.  Measured: c2mod
+// apply 0.0345 -> 0.0318 ms, c3h 0.1006 -> 0.0905, c4h 0.3421 -> 0.3297, c5 neutral.  (Triggering
+// at CTA start instead measured slower on the large grids: c4h 0.369, c5 +10%.)  IE_PDL=0 turns
+// it off.
+static bool use_pdl(const ApplyParams&) {
   static const int env = [] {
     const char* v = getenv("IE_PDL");
-    return v ? atoi(v) : -1;
+    return v ? atoi(v) : 1;
   }();
-  if (env >= 0) return env != 0;
-  return (long long)p.nx * p.ny * p.nz * p.n_items <= (1LL << 18);
+  return env != 0;
 }
 template <typename... Args>
 static void launch_pass(bool pdl, void (*kernel)(Args...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
