@@ -22,31 +22,13 @@
 
 #include "bulk_copy.cuh"
 #include "fft_core.cuh"
+#include "pdl.cuh"
 #include "ie_internal.h"
 
 namespace ie {
 
 __device__ __forceinline__ double2 ld2(const double2* p) { return __ldg(p); }
 
-#ifndef IE_PDL_LATE
-#define IE_PDL_LATE 1  // 0: trigger the dependent pass at CTA start instead of CTA exit (A/B build)
-#endif
-// Programmatic dependent launch (launch_pass): a pass launched with the PDL attribute may be
-// scheduled before the previous pass has finished; every global access of the pass comes after
-// pdl_wait(), which returns once the previous grid has completed and its writes are visible (a
-// no-op without the attribute).  The trigger that lets the next pass's CTAs be scheduled is issued
-// as each CTA finishes (pdl_trigger_late), so they take the SMs the exiting CTAs free.
-__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
-__device__ __forceinline__ void pdl_trigger() {
-#if !IE_PDL_LATE
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-#endif
-}
-__device__ __forceinline__ void pdl_trigger_late() {
-#if IE_PDL_LATE
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-#endif
-}
 
 
 // =====================================================================  K-A
@@ -298,6 +280,7 @@ __device__ __forceinline__ double2 cdot3(double2 g0, double2 j0, double2 g1, dou
 
 template <int L, int W>
 __global__ void __launch_bounds__(128, 2) k_zconv16(const __grid_constant__ ApplyParams p) {
+  pdl_wait();
   constexpr int T = L / 16, R1 = L / 16, U = 16 / R1, NZ = L / 2;
   static_assert(L == 64 || L == 128 || L == 256, "radix-16 z-pass: L in {64,128,256}");
   extern __shared__ __align__(16) double2 sm[];
@@ -466,6 +449,7 @@ __global__ void __launch_bounds__(128, 2) k_zconv16(const __grid_constant__ Appl
 #pragma unroll
     for (int r = 0; r < 8; ++r) dst[(long long)(t + r * T) * zs] = v[r];  // z = t + r L/16 < nz
   }
+  pdl_trigger_late();
 }
 
 // K-C, TMEM-parked z-pass for L = 2nz in {128, 256}: T = L/16 threads per pencil, W = 2048/L pencils per CTA (128 threads, one TMEM
@@ -1272,38 +1256,6 @@ static int rev_order() {
   return r;
 }
 
-// Launch one operator pass with the programmatic-dependent-launch attribute: the next pass's CTAs
-// are scheduled as this pass's CTAs exit (pdl_trigger_late) and wait for its completion in
-// pdl_wait, so the pass boundary costs no launch gap.  Measured: c2mod
-// apply 0.0345 -> 0.0318 ms, c3h 0.1006 -> 0.0905, c4h 0.3421 -> 0.3297, c5 neutral.  (Triggering
-// at CTA start instead measured slower on the large grids: c4h 0.369, c5 +10%.)  IE_PDL=0 turns
-// it off.
-static bool use_pdl(const ApplyParams&) {
-  static const int env = [] {
-    const char* v = getenv("IE_PDL");
-    return v ? atoi(v) : 1;
-  }();
-  return env != 0;
-}
-template <typename... Args>
-static void launch_pass(bool pdl, void (*kernel)(Args...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
-                        Args... args) {
-  if (!pdl) {
-    kernel<<<grid, block, smem, s>>>(args...);
-    return;
-  }
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = grid;
-  cfg.blockDim = block;
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = s;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, kernel, args...);
-}
 
 // x-passes: rows_cta rows of 3 lines; y-passes: W columns; z-pass: W columns of 3 lines
 static int rows_per_cta(int T) { return T >= 128 ? 1 : 128 / T; }
@@ -1342,7 +1294,7 @@ static cudaError_t go_xfwd(const ApplyParams& p, cudaStream_t s, int max_rows) {
   const size_t smem = (size_t)rows * padded(L) * sizeof(double2);
   cudaError_t e = prep((const void*)k_xfwd<L>, smem);
   if (e) return e;
-  launch_pass(use_pdl(p), k_xfwd<L>, dim3((max_rows + rows - 1) / rows, p.n_items), dim3(rows * T), smem, s, p);
+  launch_pass(use_pdl(), k_xfwd<L>, dim3((max_rows + rows - 1) / rows, p.n_items), dim3(rows * T), smem, s, p);
   return cudaGetLastError();
 }
 template <int L>
@@ -1353,7 +1305,7 @@ static cudaError_t go_yfwd(const ApplyParams& p, cudaStream_t s, int max_planes)
   if (e) return e;
   ApplyParams q = p;
   q.rev = rev_order();
-  launch_pass(use_pdl(p), k_yfwd<L>, dim3(p.x2w / W, max_planes, 3 * p.n_items), dim3(W * T), smem, s, q);
+  launch_pass(use_pdl(), k_yfwd<L>, dim3(p.x2w / W, max_planes, 3 * p.n_items), dim3(W * T), smem, s, q);
   return cudaGetLastError();
 }
 template <int L>
@@ -1378,7 +1330,7 @@ static cudaError_t go_zconv16_w(const ApplyParams& p, cudaStream_t s) {
   const size_t smem = (size_t)(3 * L * W + L) * sizeof(double2);
   cudaError_t e = prep((const void*)k_zconv16<L, W>, smem);
   if (e) return e;
-  k_zconv16<L, W><<<dim3(p.n_items * (p.x2w / W), 2 * p.ny), W * (L / 16), smem, s>>>(p);
+  launch_pass(use_pdl(), k_zconv16<L, W>, dim3(p.n_items * (p.x2w / W), 2 * p.ny), dim3(W * (L / 16)), smem, s, p);
   return cudaGetLastError();
 }
 template <int L, bool HT, bool PM, bool FM>
@@ -1387,7 +1339,7 @@ static cudaError_t go_zconv_tm_h(const ApplyParams& p, cudaStream_t s) {
   const size_t smem = (size_t)(4 * (L / 2) * W + L + 1) * sizeof(double2);
   cudaError_t e = prep((const void*)k_zconv_tm<L, HT, PM, FM>, smem);
   if (e) return e;
-  launch_pass(use_pdl(p), k_zconv_tm<L, HT, PM, FM>, dim3(p.n_items * (p.x2w / W), 2 * p.ny), dim3(128), smem, s, p);
+  launch_pass(use_pdl(), k_zconv_tm<L, HT, PM, FM>, dim3(p.n_items * (p.x2w / W), 2 * p.ny), dim3(128), smem, s, p);
   return cudaGetLastError();
 }
 template <int L>
@@ -1446,7 +1398,7 @@ static cudaError_t go_yinv(const ApplyParams& p, cudaStream_t s) {
   const size_t smem = (size_t)padded(L * W) * sizeof(double2);
   cudaError_t e = prep((const void*)k_yinv<L>, smem);
   if (e) return e;
-  launch_pass(use_pdl(p), k_yinv<L>, dim3(p.x2w / W, p.nz, 3 * p.n_items), dim3(W * T), smem, s, p);
+  launch_pass(use_pdl(), k_yinv<L>, dim3(p.x2w / W, p.nz, 3 * p.n_items), dim3(W * T), smem, s, p);
   return cudaGetLastError();
 }
 template <int L, bool PRE>
@@ -1457,7 +1409,7 @@ static cudaError_t go_xinv_p(const ApplyParams& p, cudaStream_t s) {
   if (e) return e;
   ApplyParams q = p;
   q.rev = rev_order();
-  launch_pass(use_pdl(p), k_xinv<L, PRE>, dim3((p.ny * p.nz + rows - 1) / rows, 3 * p.n_items), dim3(rows * T), smem, s, q);
+  launch_pass(use_pdl(), k_xinv<L, PRE>, dim3((p.ny * p.nz + rows - 1) / rows, 3 * p.n_items), dim3(rows * T), smem, s, q);
   return cudaGetLastError();
 }
 template <int L>
