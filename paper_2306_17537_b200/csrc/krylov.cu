@@ -16,6 +16,7 @@
 
 #include "fft_core.cuh"
 #include "ie_internal.h"
+#include "pdl.cuh"
 
 namespace ie {
 
@@ -46,9 +47,7 @@ __device__ __forceinline__ double2 shfl_down2(double2 v, int d) {
 // are issued before the FMAs (uniform predicates, no divergence) so each thread keeps
 // (G+1) x 16 bytes in flight; two elements per thread per trip for more memory parallelism.
 template <int G>
-__global__ void __launch_bounds__(256) k_mdot(const DotJob* __restrict__ jobs, long long len, double2* __restrict__ part,
-                                              int nblk) {
-  const DotJob jb = jobs[blockIdx.z];
+__device__ __forceinline__ void mdot_body(const DotJob& jb, long long len, double2* __restrict__ part, int nblk) {
   const int g0 = blockIdx.y * G;
   if (g0 > jb.nv) return;
   if (jb.enable && *jb.enable == 0) return;
@@ -99,7 +98,28 @@ __global__ void __launch_bounds__(256) k_mdot(const DotJob* __restrict__ jobs, l
   }
 }
 
+template <int G>
+__global__ void __launch_bounds__(256) k_mdot(const DotJob* __restrict__ jobs, long long len, double2* __restrict__ part,
+                                              int nblk) {
+  mdot_body<G>(jobs[blockIdx.z], len, part, nblk);
+}
+
+// the same with the jobs passed by value (no job upload before the launch, so the multi-dot
+// follows the operator's last pass in the programmatic-dependent-launch chain, pdl.cuh)
+constexpr int kMaxDotJobs = 64;
+struct DotJobs {
+  DotJob j[kMaxDotJobs];
+};
+template <int G>
+__global__ void __launch_bounds__(256) k_mdot_val(const __grid_constant__ DotJobs jobs, long long len,
+                                                  double2* __restrict__ part, int nblk) {
+  pdl_wait();
+  mdot_body<G>(jobs.j[blockIdx.z], len, part, nblk);
+  pdl_trigger_late();
+}
+
 __global__ void k_reduce_rows(const double2* __restrict__ part, int nblk, double2* __restrict__ out) {
+  pdl_wait();
   const int row = blockIdx.x;
   __shared__ double2 red[128];
   double2 s = czero();
@@ -111,6 +131,7 @@ __global__ void k_reduce_rows(const double2* __restrict__ part, int nblk, double
     __syncthreads();
   }
   if (threadIdx.x == 0) out[row] = red[0];
+  pdl_trigger_late();
 }
 
 // out = base + sum_j coef_j V_j.  Eight basis loads of an element are issued before their FMAs
@@ -536,12 +557,19 @@ ie_status gmres_batched(ie_ctx* c, Arena& ar, int nx, int ny, int nz, int k0, lo
       rowbase[i] = row;
       row += nv[i] + 1;
     }
-    IE_CUDA(c, cudaMemcpyAsync(d_dot, hj, n * sizeof(DotJob), cudaMemcpyHostToDevice, c->stream));
     int maxnv = 0;
     for (int i = 0; i < n; ++i) maxnv = std::max(maxnv, nv[i]);
-    k_mdot<kDotG><<<dim3(nblk, maxnv / kDotG + 1, n), 256, 0, c->stream>>>(d_dot, len, part, nblk);
+    if (n <= kMaxDotJobs) {
+      DotJobs dj;
+      for (int i = 0; i < n; ++i) dj.j[i] = hj[i];
+      launch_pass(use_pdl(), k_mdot_val<kDotG>, dim3(nblk, maxnv / kDotG + 1, n), dim3(256), 0, c->stream, dj, len, part,
+                  nblk);
+    } else {
+      IE_CUDA(c, cudaMemcpyAsync(d_dot, hj, n * sizeof(DotJob), cudaMemcpyHostToDevice, c->stream));
+      k_mdot<kDotG><<<dim3(nblk, maxnv / kDotG + 1, n), 256, 0, c->stream>>>(d_dot, len, part, nblk);
+    }
     IE_CHECK_LAUNCH(c, "k_mdot");
-    k_reduce_rows<<<row, 128, 0, c->stream>>>(part, nblk, rows);
+    launch_pass(use_pdl(), k_reduce_rows, dim3(row), dim3(128), 0, c->stream, (const double2*)part, nblk, rows);
     IE_CHECK_LAUNCH(c, "k_reduce_rows");
     IE_CUDA(c, cudaMemcpyAsync(hrows, rows, row * sizeof(double2), cudaMemcpyDeviceToHost, c->stream));
     IE_CUDA(c, cudaStreamSynchronize(c->stream));
@@ -955,18 +983,17 @@ ie_status vec_dots(ie_ctx* c, Arena& ar, const double2* w, const double2* V, int
                    double* wn2) {
   const int nblk = dot_blocks(1);
   const size_t mark = ar.used;
-  DotJob* dj = (DotJob*)ar.take(sizeof(DotJob));
   double2* part = (double2*)ar.take((size_t)(nv + 1) * nblk * sizeof(double2));
   double2* rows = (double2*)ar.take((size_t)(nv + 1) * sizeof(double2));
-  if (!dj || !part || !rows) {
+  if (!part || !rows) {
     ar.used = mark;
     return fail(c, IE_ERR_OUT_OF_MEMORY, "workspace too small for the outer Krylov basis");
   }
-  const DotJob hj{w, V, nv, 0};
-  IE_CUDA(c, cudaMemcpyAsync(dj, &hj, sizeof(DotJob), cudaMemcpyHostToDevice, c->stream));
-  k_mdot<kDotG><<<dim3(nblk, nv / kDotG + 1, 1), 256, 0, c->stream>>>(dj, len, part, nblk);
+  DotJobs jobs;
+  jobs.j[0] = DotJob{w, V, nv, 0};
+  launch_pass(use_pdl(), k_mdot_val<kDotG>, dim3(nblk, nv / kDotG + 1, 1), dim3(256), 0, c->stream, jobs, len, part, nblk);
   IE_CHECK_LAUNCH(c, "k_mdot");
-  k_reduce_rows<<<nv + 1, 128, 0, c->stream>>>(part, nblk, rows);
+  launch_pass(use_pdl(), k_reduce_rows, dim3(nv + 1), dim3(128), 0, c->stream, (const double2*)part, nblk, rows);
   IE_CHECK_LAUNCH(c, "k_reduce_rows");
   std::vector<double2> hr(nv + 1);
   IE_CUDA(c, cudaMemcpyAsync(hr.data(), rows, (nv + 1) * sizeof(double2), cudaMemcpyDeviceToHost, c->stream));
