@@ -136,10 +136,8 @@ __global__ void k_reduce_rows(const double2* __restrict__ part, int nblk, double
 
 // out = base + sum_j coef_j V_j.  Eight basis loads of an element are issued before their FMAs
 // (uniform predicates) so each thread keeps 8 x 16 bytes in flight.
-__global__ void __launch_bounds__(256) k_maxpy(const AxpyJob* __restrict__ jobs, const double2* __restrict__ coefs,
-                                               long long len) {
+__device__ __forceinline__ void maxpy_body(const AxpyJob& jb, const double2* __restrict__ coefs, long long len) {
   constexpr int G = 8;
-  const AxpyJob jb = jobs[blockIdx.y];
   if (jb.enable && *jb.enable == 0) return;
   __shared__ double2 cf[160];
   for (int j = threadIdx.x; j < jb.nv; j += blockDim.x) cf[j] = coefs[jb.coef + j];
@@ -158,6 +156,21 @@ __global__ void __launch_bounds__(256) k_maxpy(const AxpyJob* __restrict__ jobs,
     }
     jb.out[i] = cadd(a0, a1);
   }
+}
+__global__ void __launch_bounds__(256) k_maxpy(const AxpyJob* __restrict__ jobs, const double2* __restrict__ coefs,
+                                               long long len) {
+  maxpy_body(jobs[blockIdx.y], coefs, len);
+}
+// the same with jobs and coefficients passed by value (no upload before the launch; pdl.cuh)
+constexpr int kMaxAxpyJobs = 16, kMaxAxpyCoefs = 256;
+struct AxpyPack {
+  AxpyJob j[kMaxAxpyJobs];
+  double2 cf[kMaxAxpyCoefs];
+};
+__global__ void __launch_bounds__(256) k_maxpy_val(const __grid_constant__ AxpyPack pk, long long len) {
+  pdl_wait();
+  maxpy_body(pk.j[blockIdx.y], pk.cf, len);
+  pdl_trigger_late();
 }
 
 // ------------------------------------------------------- device-side Arnoldi recurrences
@@ -579,11 +592,19 @@ ie_status gmres_batched(ie_ctx* c, Arena& ar, int nx, int ny, int nz, int k0, lo
   auto axpy = [&](const std::vector<AxpyJob>& jobs, const std::vector<cplx>& coefs) -> ie_status {
     const int n = (int)jobs.size();
     if (n == 0) return IE_OK;
+    const int gx = (int)std::max<long long>(1, std::min<long long>((len + 255) / 256, 1184 / n + 1));
+    if (n <= kMaxAxpyJobs && coefs.size() <= (size_t)kMaxAxpyCoefs) {
+      AxpyPack pk;
+      for (int i = 0; i < n; ++i) pk.j[i] = jobs[i];
+      for (size_t i = 0; i < coefs.size(); ++i) pk.cf[i] = make_double2(coefs[i].real(), coefs[i].imag());
+      launch_pass(use_pdl(), k_maxpy_val, dim3(gx, n), dim3(256), 0, c->stream, pk, len);
+      IE_CHECK_LAUNCH(c, "k_maxpy");
+      return IE_OK;
+    }
     for (int i = 0; i < n; ++i) h_axpy[i] = jobs[i];
     for (size_t i = 0; i < coefs.size(); ++i) h_coef[i] = make_double2(coefs[i].real(), coefs[i].imag());
     IE_CUDA(c, cudaMemcpyAsync(d_axpy, h_axpy, n * sizeof(AxpyJob), cudaMemcpyHostToDevice, c->stream));
     IE_CUDA(c, cudaMemcpyAsync(d_coef, h_coef, coefs.size() * sizeof(double2), cudaMemcpyHostToDevice, c->stream));
-    const int gx = (int)std::max<long long>(1, std::min<long long>((len + 255) / 256, 1184 / n + 1));
     k_maxpy<<<dim3(gx, n), 256, 0, c->stream>>>(d_axpy, d_coef, len);
     IE_CHECK_LAUNCH(c, "k_maxpy");
     return IE_OK;
