@@ -24,6 +24,7 @@
 #include "bulk_copy.cuh"
 #include "fft_core.cuh"
 #include "ie_internal.h"
+#include "pdl.cuh"
 #include "kernel_eval.cuh"
 
 namespace ie {
@@ -157,6 +158,7 @@ ie_status build_layer_spec(ie_ctx* c, int bx, int by, int bz, int k0, GreenSpec*
 // over the source rows k' in [sz0, sz1) (a source-restricted apply reads less of M).
 template <int NI>
 __global__ void __launch_bounds__(256) k_zlayer(const __grid_constant__ ApplyParams p) {
+  pdl_wait();
   constexpr int NS = 4 * NI;  // column slots: (cy*2 + cx)*NI + item
   extern __shared__ __align__(16) double2 xs[];
   const int nx = p.nx, ny = p.ny, nz = p.nz, Lx = 2 * nx, Ly = 2 * ny, R = 3 * nz;
@@ -206,6 +208,7 @@ __global__ void __launch_bounds__(256) k_zlayer(const __grid_constant__ ApplyPar
       }
     }
   }
+  pdl_trigger_late();
 }
 
 // The same contraction on the FP64 tensor cores (DMMA, mma.sync m8n8k4 f64) when the
@@ -222,6 +225,7 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
 
 template <int NI>
 __global__ void __launch_bounds__(256) k_zlayer_mma(const __grid_constant__ ApplyParams p) {
+  pdl_wait();
   constexpr int NS = 4 * NI, NT = (NS + 7) / 8, NSP = NT * 8;
   extern __shared__ __align__(16) double2 xs[];  // [R][NSP], signs applied, zero padded
   const int nx = p.nx, ny = p.ny, nz = p.nz, Lx = 2 * nx, Ly = 2 * ny, R = 3 * nz;
@@ -277,6 +281,7 @@ __global__ void __launch_bounds__(256) k_zlayer_mma(const __grid_constant__ Appl
         }
       }
   }
+  pdl_trigger_late();
 }
 
 // Warp-specialised version: a producer warp streams M(ix,iy) into a 2-stage shared ring with
@@ -289,6 +294,7 @@ __global__ void __launch_bounds__(256) k_zlayer_mma(const __grid_constant__ Appl
 // so Y_s = (C1[2s] - C2[2s+1]) + i (C1[2s+1] + C2[2s]) in registers.
 template <int NI, int RT>
 __global__ void __launch_bounds__(288, 2) k_zlayer_tma(const __grid_constant__ ApplyParams p) {
+  pdl_wait();
   constexpr int NS = 4 * NI, NT = NI;      // slots; real columns 2 NS = 8 NI: NI n-tiles
   // k-rows per chunk, ring stages (3 for one RHS, where the consumers outpace a 2-deep ring;
   // 2 otherwise: c3h 1 RHS 0.517 -> 0.506 ms, 3 RHS 0.735 vs 0.760 ms), consumer warps
@@ -418,6 +424,7 @@ __global__ void __launch_bounds__(288, 2) k_zlayer_tma(const __grid_constant__ A
       }
     }
   }
+  pdl_trigger_late();
 }
 
 template <int NI, int RT>
@@ -430,7 +437,7 @@ static cudaError_t go_zlayer_tma(const ApplyParams& p, cudaStream_t s) {
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e) return e;
   }
-  k_zlayer_tma<NI, RT><<<(p.nx + 1) * (p.ny + 1), 288, smem, s>>>(p);
+  launch_pass(use_pdl(), k_zlayer_tma<NI, RT>, dim3((p.nx + 1) * (p.ny + 1)), dim3(288), smem, s, p);
   return cudaGetLastError();
 }
 
@@ -454,7 +461,7 @@ static cudaError_t go_zlayer_mma(const ApplyParams& p, cudaStream_t s) {
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e) return e;
   }
-  k_zlayer_mma<NI><<<(p.nx + 1) * (p.ny + 1), 256, smem, s>>>(p);
+  launch_pass(use_pdl(), k_zlayer_mma<NI>, dim3((p.nx + 1) * (p.ny + 1)), dim3(256), smem, s, p);
   return cudaGetLastError();
 }
 
@@ -468,7 +475,7 @@ static cudaError_t go_zlayer(const ApplyParams& p, cudaStream_t s) {
   }
   const int R = 3 * p.nz;
   const int threads = std::min(256, ((R + 31) / 32) * 32);
-  k_zlayer<NI><<<(p.nx + 1) * (p.ny + 1), threads, smem, s>>>(p);
+  launch_pass(use_pdl(), k_zlayer<NI>, dim3((p.nx + 1) * (p.ny + 1)), dim3(threads), smem, s, p);
   return cudaGetLastError();
 }
 
